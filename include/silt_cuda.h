@@ -1,0 +1,215 @@
+/*
+ * silt_cuda.h — C ABI of the B200-native time-stepping path for the coupled
+ * shallow-water + Exner (Grass bedload) relaxation solver of arXiv 1307.0491.
+ *
+ * This is the drop-in boundary.  Every entry point takes plain pointers and
+ * sizes; nothing here mentions torch, std::vector or CUDA types (streams are
+ * passed as `void*` holding a cudaStream_t).  Each function returns a status
+ * code (SILT_OK == 0); the message of the last failure on the calling thread
+ * is available from silt_last_error().  The C++ shim
+ * (paper_1307_0491_b200/csrc/silt_api.hpp) maps the codes back onto the
+ * reference's exception types.
+ *
+ * Reference interfaces replaced (paths relative to the reference checkout
+ * proj/core/):
+ *   silt_problem / silt_bc ......... Grid, Physics, BedloadLaw, BoundarySpec,
+ *                                    Scenario (include/silt/grid.hpp:12-27,
+ *                                    physics.hpp:7-11, bedload.hpp:32-52,
+ *                                    scenarios.hpp:24-49)
+ *   silt_solver_create/upload ...... PaddedField::from_field, partition
+ *                                    (src/stepper.cpp:13-18, src/parallel.cpp:150-177)
+ *   silt_solver_begin .............. run_serial/run_parallel prologue + first
+ *                                    cfl_dt (src/parallel.cpp:208-222, 261-316;
+ *                                    src/stepper.cpp:38-58)
+ *   silt_solver_step ............... one loop trip of run_serial/run_parallel:
+ *                                    apply_bcs + cfl_dt + clip + step_2d/step_1d
+ *                                    (src/parallel.cpp:221-250, 315-364;
+ *                                    src/stepper.cpp:118-189; src/scenarios.cpp:78-144)
+ *   silt_solver_reduce_slot /
+ *   silt_solver_exchange_ptrs ...... global_dt + halo_exchange/pull_halo
+ *                                    (src/parallel.cpp:43-99, 192-206)
+ *   silt_solver_download ........... PaddedField::interior, gather
+ *                                    (src/stepper.cpp:20-25, src/parallel.cpp:179-190)
+ *   silt_run ....................... run_serial (src/parallel.cpp:208-259)
+ *   silt_cfl_dt .................... cfl_dt (include/silt/stepper.hpp:38-41)
+ *   silt_step_padded ............... step_1d / step_2d on a halo-complete
+ *                                    PaddedField (include/silt/stepper.hpp:47-54)
+ *   silt_riemann_batch ............. equilibrate + celerity_bounds +
+ *                                    interface_riemann (relax_state.hpp:27-51,
+ *                                    riemann.hpp:33-35)
+ */
+#ifndef SILT_CUDA_H
+#define SILT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SILT_ABI_VERSION 1
+
+/* Status codes.  INVALID ~ std::invalid_argument, RUNTIME ~ std::runtime_error
+ * in the reference (SURVEY §8b "Errors"). */
+enum {
+    SILT_OK = 0,
+    SILT_ERR_INVALID = 1,
+    SILT_ERR_RUNTIME = 2,
+    SILT_ERR_CUDA = 3,
+    SILT_ERR_UNSUPPORTED = 4
+};
+
+/* BcType, in the reference's enum order (include/silt/scenarios.hpp:17-22),
+ * plus GIVEN: ghosts supplied by the caller (halo-complete PaddedField). */
+enum {
+    SILT_BC_INFLOW = 0,
+    SILT_BC_OUTFLOW = 1,
+    SILT_BC_WALL = 2,
+    SILT_BC_PERIODIC = 3,
+    SILT_BC_GIVEN = 4
+};
+
+/* Side order of Scenario::bc (include/silt/scenarios.hpp:15). */
+enum { SILT_WEST = 0, SILT_EAST = 1, SILT_SOUTH = 2, SILT_NORTH = 3 };
+
+/* Numerical variant of the kernels. FAST: contracted FMAs, reciprocals,
+ * closed-form Grass terms; parity to 1e-9 normwise.  STRICT: the reference's
+ * operation order, no FMA contraction, IEEE division and a correctly rounded
+ * hypot (bitwise-comparable with the CPU reference). */
+enum { SILT_VARIANT_FAST = 0, SILT_VARIANT_STRICT = 1 };
+
+/* Run state reported by silt_solver_status. */
+enum {
+    SILT_STATE_RUNNING = 0,  /* more steps would advance the run */
+    SILT_STATE_DONE = 1,     /* t >= t_end or steps >= max_steps */
+    SILT_STATE_PAUSED = 2,   /* landed on a snapshot time; call silt_solver_resume */
+    SILT_STATE_FAILED = 3    /* a step raised an error (see error_code) */
+};
+
+typedef struct silt_bc {
+    int32_t type;          /* SILT_BC_* */
+    int32_t supercritical; /* Inflow: impose h0 as well */
+    double q0;             /* Inflow: imposed normal discharge */
+    double h0;             /* Inflow (supercritical): imposed depth */
+} silt_bc;
+
+/* One configured problem: grid + physics + Grass law + BCs + run knobs. */
+typedef struct silt_problem {
+    int32_t dim;       /* 1 or 2 */
+    int32_t nx, ny;    /* global cell counts (ny == 1 in 1D) */
+    int32_t law_kind;  /* 0 = Grass; anything else is rejected (Shields out of scope) */
+    double dx, dy;     /* Grid::dx, Grid::dy (1D: dy = 1) */
+    double gravity;    /* Physics::gravity */
+    double h_dry;      /* Physics::h_dry */
+    double a_g, m_g;   /* BedloadLaw::grass(a_g, m_g) */
+    double cfl;        /* Scenario::cfl, in (0, 1] */
+    double safety;     /* Scenario::safety (>= 1) */
+    silt_bc bc[4];     /* West, East, South, North */
+} silt_problem;
+
+/* Which rows of the global grid one solver owns (row strips, px = 1). */
+typedef struct silt_strip {
+    int32_t j0;              /* global index of local row 0 */
+    int32_t ny_local;        /* rows owned */
+    int32_t south_neighbor;  /* 1: ghost row -1 arrives from another strip */
+    int32_t north_neighbor;  /* 1: ghost row ny_local arrives from another strip */
+} silt_strip;
+
+typedef struct silt_run_plan {
+    double t_end;                 /* >= 0; +inf allowed */
+    int64_t max_steps;            /* < 0: unlimited */
+    const double* snapshot_times; /* host array, may be NULL */
+    int32_t n_snapshots;
+    int64_t dt_log_capacity;      /* device-side dt log length (0: none) */
+} silt_run_plan;
+
+typedef struct silt_status {
+    double t;            /* simulated time reached */
+    int64_t steps;       /* steps taken */
+    int32_t state;       /* SILT_STATE_* */
+    int32_t error_code;  /* SILT_OK or SILT_ERR_* when state == FAILED */
+    double last_dt;      /* dt of the last step taken */
+    int32_t snapshot_index; /* snapshots landed so far */
+    int32_t pad_;
+} silt_status;
+
+/* Device pointers a multi-rank driver moves between strips after each step
+ * (4 fields h,hu,hv,zb packed as [4][nx] doubles).  send_* are written by the
+ * step kernel; recv_* are read by the next step.  NULL when the side has no
+ * neighbour. */
+typedef struct silt_exchange {
+    double* send_south;
+    double* send_north;
+    double* recv_south;
+    double* recv_north;
+    int64_t row_doubles; /* 4 * nx */
+} silt_exchange;
+
+typedef struct silt_solver silt_solver;
+
+int silt_abi_version(void);
+const char* silt_last_error(void);
+int silt_device_count(int* count);
+
+/* ---- solver handle ------------------------------------------------------ */
+int silt_solver_create(const silt_problem* problem, const silt_strip* strip,
+                       int device, int variant, silt_solver** out);
+int silt_solver_destroy(silt_solver* s);
+int silt_solver_set_stream(silt_solver* s, void* cuda_stream);
+/* AoS FlowState {h,hu,hv,zb} rows of this strip, ny_local * nx cells; host
+ * pointer (pinned or pageable). */
+int silt_solver_upload(silt_solver* s, const double* host_aos);
+int silt_solver_download(silt_solver* s, double* host_aos);
+/* Same with device pointers (AoS, nx*ny_local*4 doubles). */
+int silt_solver_upload_device(silt_solver* s, const double* dev_aos);
+int silt_solver_download_device(silt_solver* s, double* dev_aos);
+/* Caller-supplied ghost cells (SILT_BC_GIVEN sides): AoS, west/east ny_local
+ * cells, south/north nx cells; any pointer may be NULL. */
+int silt_solver_set_ghosts(silt_solver* s, const double* west, const double* east,
+                           const double* south, const double* north);
+/* Reset the run clock to t = 0 and reduce state 0 (first cfl_dt). Async. */
+int silt_solver_begin(silt_solver* s, const silt_run_plan* plan);
+/* Enqueue n predicated steps (async; no host synchronisation). */
+int silt_solver_step(silt_solver* s, int n);
+/* One step with a caller-chosen dt (step_1d/step_2d semantics, no clipping). */
+int silt_solver_step_fixed(silt_solver* s, double dt);
+/* Synchronise and read the run state; returns the error of a failed step. */
+int silt_solver_status(silt_solver* s, silt_status* st);
+/* Continue after a snapshot pause. */
+int silt_solver_resume(silt_solver* s);
+/* dt of steps [0, n) from the device log (n <= capacity). */
+int silt_solver_dt_log(silt_solver* s, double* host_out, int64_t n);
+/* Current cfl_dt of the uploaded state (synchronises). */
+int silt_solver_cfl_dt(silt_solver* s, double* dt);
+/* Multi-rank hooks. reduce_slot: device pointer to the {max_x, max_y} axis
+ * speeds the NEXT step reads; a driver all-reduces it with MAX (per step, in
+ * stream order) before enqueueing that step. */
+int silt_solver_reduce_slot(silt_solver* s, double** dev_ptr);
+int silt_solver_exchange_ptrs(silt_solver* s, silt_exchange* out);
+/* Number of kernel launches this handle has enqueued (for accounting). */
+int silt_solver_launch_count(silt_solver* s, int64_t* count);
+
+/* ---- one-shot conveniences (mirror the reference free functions) ---------- */
+/* run_serial: whole run on one GPU; host AoS in/out; dt_log may be NULL. */
+int silt_run(const silt_problem* problem, const double* init_aos,
+             const silt_run_plan* plan, int variant, double* out_aos,
+             double* dt_log, int64_t dt_log_capacity, silt_status* status);
+/* cfl_dt over an interior field (AoS nx*ny). */
+int silt_cfl_dt(const silt_problem* problem, const double* field_aos,
+                int variant, double* dt);
+/* step_1d/step_2d on a halo-complete padded field (AoS (nx+2)*(ny+2), ghost
+ * frame included; 1D: 3 rows, the middle one used). In place. */
+int silt_step_padded(const silt_problem* problem, double* padded_aos,
+                     double dt, int variant);
+/* Batch of interface solves: cells L[n][4], R[n][4] (FlowState h,hu,hv,zb),
+ * axis 0 = X / 1 = Y.  out[n][5] = {F_h, F_hu_left, F_hu_right, F_hv, F_z}
+ * (the reference FaceFlux, src/stepper.cpp:61-89). */
+int silt_riemann_batch(const silt_problem* problem, const double* left,
+                       const double* right, int64_t n, int axis, int variant,
+                       double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SILT_CUDA_H */
