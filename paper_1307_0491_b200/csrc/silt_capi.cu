@@ -1,0 +1,702 @@
+// silt_capi.cu — host runtime behind include/silt_cuda.h.
+//
+// Owns device memory (SoA ping-pong planes, ghost rows, the Control block),
+// validates problems with the reference's messages, enqueues the fused step
+// kernels on the solver's stream and maps device error words back onto the
+// reference's exception classes (status codes SILT_ERR_INVALID ~
+// std::invalid_argument, SILT_ERR_RUNTIME ~ std::runtime_error).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "silt_cuda.h"
+#include "silt_launch.h"
+#include "silt_layout.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(SILT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_));     \
+    } while (0)
+
+__global__ void aos_to_soa(const double* __restrict__ aos, double* h, double* hu, double* hv,
+                           double* zb, int nx, int ny, int pitch) {
+    const long long n = (long long)nx * ny;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double4 c = reinterpret_cast<const double4*>(aos)[k];
+        const long long off = (k / nx) * pitch + (k % nx);
+        h[off] = c.x;
+        hu[off] = c.y;
+        hv[off] = c.z;
+        zb[off] = c.w;
+    }
+}
+
+__global__ void soa_to_aos(double* __restrict__ aos, const double* h, const double* hu,
+                           const double* hv, const double* zb, int nx, int ny, int pitch) {
+    const long long n = (long long)nx * ny;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long off = (k / nx) * pitch + (k % nx);
+        reinterpret_cast<double4*>(aos)[k] = make_double4(h[off], hu[off], hv[off], zb[off]);
+    }
+}
+
+// AoS ghost cells (n cells) -> [4][n] planes
+__global__ void aos_to_planes(const double* __restrict__ aos, double* planes, int n) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    for (int f = 0; f < 4; ++f) planes[(size_t)f * n + k] = aos[4 * (size_t)k + f];
+}
+
+int grid_blocks(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return (int)std::max(1LL, std::min(b, 148LL * 32));
+}
+
+const char* kNegDepthMsg =
+    "step: negative depth produced; time step or celerities violate stability";
+
+}  // namespace
+
+struct silt_solver {
+    silt_problem prob{};
+    silt_strip strip{};
+    int device = 0;
+    int variant = SILT_VARIANT_FAST;
+    int nx = 0, ny = 0, pitch = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double* planes = nullptr;   // [2][4][ny][pitch]
+    double* rows = nullptr;     // 8 x [4][nx]
+    double* cols = nullptr;     // 2 x [4][ny]
+    double* staging = nullptr;  // AoS nx*ny*4
+    Control* ctl = nullptr;
+    Control* host_ctl = nullptr;  // pinned staging for control uploads
+    double* dt_log = nullptr;
+    int64_t dt_cap = 0;
+    double* snaps = nullptr;
+    int n_snaps_alloc = 0;
+    int64_t launches = 0;
+    int64_t kernel_count = 0;
+    bool begun = false;
+    StepArgs args{};
+    dim3 step_grid;
+};
+
+namespace {
+
+int validate_problem(const silt_problem* p) {
+    if (!p) return fail(SILT_ERR_INVALID, "silt: null problem");
+    if (p->dim != 1 && p->dim != 2) return fail(SILT_ERR_INVALID, "grid: dim must be 1 or 2");
+    if (p->nx < 1) return fail(SILT_ERR_INVALID, "grid: cell count nx must be >= 1");
+    if (p->dim == 2 && p->ny < 1) return fail(SILT_ERR_INVALID, "grid: cell count ny must be >= 1");
+    if (!(p->dx > 0) || !std::isfinite(p->dx))
+        return fail(SILT_ERR_INVALID, "grid: length_x must be positive");
+    if (p->dim == 2 && (!(p->dy > 0) || !std::isfinite(p->dy)))
+        return fail(SILT_ERR_INVALID, "grid: length_y must be positive");
+    if (p->law_kind != 0)
+        return fail(SILT_ERR_UNSUPPORTED,
+                    "bedload: only the Grass law is implemented on the GPU path");
+    if (!(p->a_g >= 0) || !std::isfinite(p->a_g))
+        return fail(SILT_ERR_INVALID, "bedload: Grass a_g must be >= 0");
+    if (!(p->m_g >= 1.0 && p->m_g <= 4.0))
+        return fail(SILT_ERR_INVALID, "bedload: Grass m_g must lie in [1, 4]");
+    const bool px0 = p->bc[SILT_WEST].type == SILT_BC_PERIODIC;
+    const bool px1 = p->bc[SILT_EAST].type == SILT_BC_PERIODIC;
+    if (px0 != px1) return fail(SILT_ERR_INVALID, "apply_bcs: periodic requires both x sides");
+    if (p->dim == 2) {
+        const bool py0 = p->bc[SILT_SOUTH].type == SILT_BC_PERIODIC;
+        const bool py1 = p->bc[SILT_NORTH].type == SILT_BC_PERIODIC;
+        if (py0 != py1) return fail(SILT_ERR_INVALID, "apply_bcs: periodic requires both y sides");
+    }
+    for (int s = 0; s < 4; ++s)
+        if (p->bc[s].type < SILT_BC_INFLOW || p->bc[s].type > SILT_BC_GIVEN)
+            return fail(SILT_ERR_INVALID, "silt: unknown boundary type");
+    return SILT_OK;
+}
+
+int check_cfl(double cfl) {
+    if (!(cfl > 0) || !(cfl <= 1)) return fail(SILT_ERR_INVALID, "cfl_dt: cfl must lie in (0, 1]");
+    return SILT_OK;
+}
+
+void launch_step(silt_solver* s) {
+    const int li = (int)(s->launches % 3);
+    if (s->variant == SILT_VARIANT_STRICT)
+        silt_strict_step(s->args, li, s->step_grid, s->stream);
+    else
+        silt_fast_step(s->args, li, s->step_grid, s->stream);
+    ++s->launches;
+    ++s->kernel_count;
+}
+
+int read_slot(silt_solver* s, Slot* out, Control* full) {
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    CUDA_TRY(cudaGetLastError());
+    if (full) {
+        CUDA_TRY(cudaMemcpy(full, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost));
+        *out = full->slot[s->launches % 3];
+    } else {
+        CUDA_TRY(cudaMemcpy(out, &s->ctl->slot[s->launches % 3], sizeof(Slot),
+                            cudaMemcpyDeviceToHost));
+    }
+    return SILT_OK;
+}
+
+int error_from(const Control& c, unsigned bits) {
+    if (bits & silt_dev::kErrRiemann) {
+        char buf[512];
+        std::snprintf(buf, sizeof buf,
+                      "interface_riemann: no positive fan after 25 celerity enlargements "
+                      "(hL=%g uL=%g zL=%g | hR=%g uR=%g zR=%g)",
+                      c.err_info[0], c.err_info[1], c.err_info[2], c.err_info[3], c.err_info[4],
+                      c.err_info[5]);
+        return fail(SILT_ERR_RUNTIME, buf);
+    }
+    if (bits & silt_dev::kErrNegDepth) return fail(SILT_ERR_RUNTIME, kNegDepthMsg);
+    if (bits & silt_dev::kErrDry) return fail(SILT_ERR_INVALID, "cfl_dt: field is entirely dry");
+    return fail(SILT_ERR_RUNTIME, "step: device error");
+}
+
+}  // namespace
+
+extern "C" {
+
+int silt_abi_version(void) { return SILT_ABI_VERSION; }
+
+const char* silt_last_error(void) { return g_err.c_str(); }
+
+int silt_device_count(int* count) {
+    CUDA_TRY(cudaGetDeviceCount(count));
+    return SILT_OK;
+}
+
+int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int device,
+                       int variant, silt_solver** out) {
+    if (!out) return fail(SILT_ERR_INVALID, "silt_solver_create: null out");
+    *out = nullptr;
+    if (int rc = validate_problem(problem)) return rc;
+    if (variant != SILT_VARIANT_FAST && variant != SILT_VARIANT_STRICT)
+        return fail(SILT_ERR_INVALID, "silt_solver_create: unknown variant");
+    const int gny = problem->dim == 1 ? 1 : problem->ny;
+    silt_strip st{0, gny, 0, 0};
+    if (strip) st = *strip;
+    if (st.ny_local < 1 || st.j0 < 0 || st.j0 + st.ny_local > gny)
+        return fail(SILT_ERR_INVALID, "partition: every worker needs at least one cell per axis");
+    if (problem->dim == 1 && (st.south_neighbor || st.north_neighbor || st.ny_local != 1))
+        return fail(SILT_ERR_INVALID, "partition: 1D grids require py == 1");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(SILT_ERR_CUDA, "silt_solver_create: bad device");
+    CUDA_TRY(cudaSetDevice(device));
+
+    silt_solver* s = new silt_solver();
+    s->prob = *problem;
+    s->prob.ny = gny;
+    s->strip = st;
+    s->device = device;
+    s->variant = variant;
+    s->nx = problem->nx;
+    s->ny = st.ny_local;
+    s->pitch = (s->nx + 31) / 32 * 32;
+    const size_t plane = (size_t)s->ny * s->pitch;
+    auto cleanup = [&](int rc) {
+        silt_solver_destroy(s);
+        return rc;
+    };
+    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(fail(SILT_ERR_CUDA, "cudaStreamCreate failed"));
+    s->own_stream = true;
+    if (cudaMalloc(&s->planes, 8 * plane * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&s->rows, 8 * 4 * (size_t)s->nx * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&s->cols, 2 * 4 * (size_t)s->ny * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&s->ctl, sizeof(Control)) != cudaSuccess ||
+        cudaMallocHost(&s->host_ctl, sizeof(Control)) != cudaSuccess)
+        return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: device allocation failed"));
+    cudaMemset(s->planes, 0, 8 * plane * sizeof(double));
+    cudaMemset(s->rows, 0, 8 * 4 * (size_t)s->nx * sizeof(double));
+    cudaMemset(s->cols, 0, 2 * 4 * (size_t)s->ny * sizeof(double));
+    cudaMemset(s->ctl, 0, sizeof(Control));
+
+    StepArgs& A = s->args;
+    A.dim = problem->dim;
+    A.nx = s->nx;
+    A.ny = s->ny;
+    A.pitch = s->pitch;
+    A.j0 = st.j0;
+    A.south_nbr = st.south_neighbor;
+    A.north_nbr = st.north_neighbor;
+    A.per_y_self = problem->dim == 2 && problem->bc[SILT_SOUTH].type == SILT_BC_PERIODIC &&
+                   !st.south_neighbor && !st.north_neighbor;
+    A.dx = problem->dx;
+    A.dy = problem->dim == 1 ? 1.0 : problem->dy;
+    A.cfl = problem->cfl;
+    A.P.g = problem->gravity;
+    A.P.h_dry = problem->h_dry;
+    A.P.a_g = problem->a_g;
+    A.P.m_g = problem->m_g;
+    A.P.safety = problem->safety;
+    A.P.half_g = 0.5 * problem->gravity;
+    A.P.m3 = problem->m_g == 3.0;
+    for (int k = 0; k < 4; ++k) {
+        A.bc_type[k] = problem->bc[k].type;
+        A.bc_super[k] = problem->bc[k].supercritical;
+        A.bc_q0[k] = problem->bc[k].q0;
+        A.bc_h0[k] = problem->bc[k].h0;
+    }
+    for (int p = 0; p < 2; ++p)
+        for (int f = 0; f < 4; ++f) A.state[p][f] = s->planes + (size_t)(p * 4 + f) * plane;
+    const size_t row = 4 * (size_t)s->nx;
+    A.ghost_s[0] = s->rows + 0 * row;
+    A.ghost_s[1] = s->rows + 1 * row;
+    A.ghost_n[0] = s->rows + 2 * row;
+    A.ghost_n[1] = s->rows + 3 * row;
+    A.recv_s = s->rows + 4 * row;
+    A.recv_n = s->rows + 5 * row;
+    A.send_s = s->rows + 6 * row;
+    A.send_n = s->rows + 7 * row;
+    A.ghost_w = s->cols;
+    A.ghost_e = s->cols + 4 * (size_t)s->ny;
+    A.ctl = s->ctl;
+    // rows per CTA: enough warps in flight for a fp64-latency-bound kernel
+    const long long strips = (s->nx + kCellsPerWarp - 1) / kCellsPerWarp;
+    long long R = (strips * s->ny + 8191) / 8192;
+    R = std::max(4LL, std::min(64LL, R));
+    if (problem->dim == 1) R = 1;
+    A.rows_per_block = (int)R;
+    const int warps_per_cta = kStepThreads / 32;
+    s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta),
+                        (unsigned)((s->ny + R - 1) / R), 1);
+    if (cudaDeviceSynchronize() != cudaSuccess)
+        return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: init failed"));
+    *out = s;
+    return SILT_OK;
+}
+
+int silt_solver_destroy(silt_solver* s) {
+    if (!s) return SILT_OK;
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    cudaFree(s->planes);
+    cudaFree(s->rows);
+    cudaFree(s->cols);
+    cudaFree(s->staging);
+    cudaFree(s->ctl);
+    cudaFree(s->dt_log);
+    cudaFree(s->snaps);
+    if (s->host_ctl) cudaFreeHost(s->host_ctl);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return SILT_OK;
+}
+
+int silt_solver_set_stream(silt_solver* s, void* stream) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    s->own_stream = false;
+    s->stream = (cudaStream_t)stream;
+    return SILT_OK;
+}
+
+static int ensure_staging(silt_solver* s) {
+    if (s->staging) return SILT_OK;
+    CUDA_TRY(cudaMalloc(&s->staging, 4 * (size_t)s->nx * s->ny * sizeof(double)));
+    return SILT_OK;
+}
+
+static int upload_impl(silt_solver* s, const double* src, cudaMemcpyKind kind) {
+    if (!s || !src) return fail(SILT_ERR_INVALID, "silt_solver_upload: null argument");
+    CUDA_TRY(cudaSetDevice(s->device));
+    if (int rc = ensure_staging(s)) return rc;
+    const size_t bytes = 4 * (size_t)s->nx * s->ny * sizeof(double);
+    CUDA_TRY(cudaMemcpyAsync(s->staging, src, bytes, kind, s->stream));
+    const StepArgs& A = s->args;
+    aos_to_soa<<<grid_blocks((long long)s->nx * s->ny, 256), 256, 0, s->stream>>>(
+        s->staging, A.state[0][0], A.state[0][1], A.state[0][2], A.state[0][3], s->nx, s->ny,
+        s->pitch);
+    ++s->kernel_count;
+    CUDA_TRY(cudaGetLastError());
+    s->begun = false;  // the run clock restarts at the uploaded state
+    return SILT_OK;
+}
+
+int silt_solver_upload(silt_solver* s, const double* host_aos) {
+    return upload_impl(s, host_aos, cudaMemcpyHostToDevice);
+}
+
+int silt_solver_upload_device(silt_solver* s, const double* dev_aos) {
+    return upload_impl(s, dev_aos, cudaMemcpyDeviceToDevice);
+}
+
+static int download_impl(silt_solver* s, double* dst, cudaMemcpyKind kind) {
+    if (!s || !dst) return fail(SILT_ERR_INVALID, "silt_solver_download: null argument");
+    CUDA_TRY(cudaSetDevice(s->device));
+    int p = 0;
+    if (s->begun) {
+        Slot sl;
+        if (int rc = read_slot(s, &sl, nullptr)) return rc;
+        p = (int)(sl.steps & 1);
+    }
+    if (int rc = ensure_staging(s)) return rc;
+    const StepArgs& A = s->args;
+    soa_to_aos<<<grid_blocks((long long)s->nx * s->ny, 256), 256, 0, s->stream>>>(
+        s->staging, A.state[p][0], A.state[p][1], A.state[p][2], A.state[p][3], s->nx, s->ny,
+        s->pitch);
+    ++s->kernel_count;
+    const size_t bytes = 4 * (size_t)s->nx * s->ny * sizeof(double);
+    CUDA_TRY(cudaMemcpyAsync(dst, s->staging, bytes, kind, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return SILT_OK;
+}
+
+int silt_solver_download(silt_solver* s, double* host_aos) {
+    return download_impl(s, host_aos, cudaMemcpyDeviceToHost);
+}
+
+int silt_solver_download_device(silt_solver* s, double* dev_aos) {
+    return download_impl(s, dev_aos, cudaMemcpyDeviceToDevice);
+}
+
+int silt_solver_set_ghosts(silt_solver* s, const double* west, const double* east,
+                           const double* south, const double* north) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    CUDA_TRY(cudaSetDevice(s->device));
+    const StepArgs& A = s->args;
+    struct Item {
+        const double* src;
+        double* dst;
+        int n;
+    } items[4] = {{west, A.ghost_w, s->ny},
+                  {east, A.ghost_e, s->ny},
+                  {south, A.ghost_s[0], s->nx},
+                  {north, A.ghost_n[0], s->nx}};
+    double* tmp = nullptr;
+    const int nmax = std::max(s->nx, s->ny);
+    CUDA_TRY(cudaMalloc(&tmp, 4 * (size_t)nmax * sizeof(double)));
+    for (auto& it : items) {
+        if (!it.src) continue;
+        cudaMemcpyAsync(tmp, it.src, 4 * (size_t)it.n * sizeof(double), cudaMemcpyHostToDevice,
+                        s->stream);
+        aos_to_planes<<<(it.n + 127) / 128, 128, 0, s->stream>>>(tmp, it.dst, it.n);
+        ++s->kernel_count;
+    }
+    cudaStreamSynchronize(s->stream);
+    cudaFree(tmp);
+    CUDA_TRY(cudaGetLastError());
+    return SILT_OK;
+}
+
+int silt_solver_begin(silt_solver* s, const silt_run_plan* plan) {
+    if (!s || !plan) return fail(SILT_ERR_INVALID, "silt_solver_begin: null argument");
+    if (!(plan->t_end >= 0)) return fail(SILT_ERR_INVALID, "run: t_end must be >= 0");
+    CUDA_TRY(cudaSetDevice(s->device));
+    // make_plan (src/parallel.cpp:101-127): keep (0, t_end], sorted, unique
+    std::vector<double> snaps;
+    for (int k = 0; k < plan->n_snapshots; ++k) {
+        const double v = plan->snapshot_times[k];
+        if (v > 0 && v <= plan->t_end) snaps.push_back(v);
+    }
+    std::sort(snaps.begin(), snaps.end());
+    snaps.erase(std::unique(snaps.begin(), snaps.end()), snaps.end());
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if ((int)snaps.size() > s->n_snaps_alloc) {
+        cudaFree(s->snaps);
+        s->snaps = nullptr;
+        CUDA_TRY(cudaMalloc(&s->snaps, snaps.size() * sizeof(double)));
+        s->n_snaps_alloc = (int)snaps.size();
+    }
+    if (!snaps.empty())
+        CUDA_TRY(cudaMemcpy(s->snaps, snaps.data(), snaps.size() * sizeof(double),
+                            cudaMemcpyHostToDevice));
+    if (plan->dt_log_capacity > s->dt_cap) {
+        cudaFree(s->dt_log);
+        s->dt_log = nullptr;
+        CUDA_TRY(cudaMalloc(&s->dt_log, plan->dt_log_capacity * sizeof(double)));
+        s->dt_cap = plan->dt_log_capacity;
+    }
+    Control& c = *s->host_ctl;
+    std::memset(&c, 0, sizeof(Control));
+    c.slot[0].state = SILT_STATE_RUNNING;
+    c.t_end = plan->t_end;
+    c.max_steps = plan->max_steps;
+    c.fixed_dt = 0;
+    c.dt_cap = std::min<int64_t>(plan->dt_log_capacity, s->dt_cap);
+    c.dt_log = s->dt_log;
+    c.snaps = s->snaps;
+    c.n_snaps = (int)snaps.size();
+    CUDA_TRY(cudaMemcpyAsync(s->ctl, &c, sizeof(Control), cudaMemcpyHostToDevice, s->stream));
+    s->launches = 0;
+    StepArgs A = s->args;
+    A.write_edges_in_reduce = 1;
+    const long long n = (long long)s->nx * s->ny;
+    if (s->variant == SILT_VARIANT_STRICT)
+        silt_strict_reduce(A, 0, grid_blocks(n, 256), s->stream);
+    else
+        silt_fast_reduce(A, 0, grid_blocks(n, 256), s->stream);
+    ++s->kernel_count;
+    CUDA_TRY(cudaGetLastError());
+    s->begun = true;
+    return SILT_OK;
+}
+
+int silt_solver_step(silt_solver* s, int n) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_step: call silt_solver_begin first");
+    if (int rc = check_cfl(s->prob.cfl)) return rc;
+    CUDA_TRY(cudaSetDevice(s->device));
+    for (int k = 0; k < n; ++k) launch_step(s);
+    CUDA_TRY(cudaGetLastError());
+    return SILT_OK;
+}
+
+int silt_solver_step_fixed(silt_solver* s, double dt) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_step_fixed: call begin first");
+    CUDA_TRY(cudaSetDevice(s->device));
+    s->host_ctl->fixed_dt = dt;
+    CUDA_TRY(cudaMemcpyAsync(&s->ctl->fixed_dt, &s->host_ctl->fixed_dt, sizeof(double),
+                             cudaMemcpyHostToDevice, s->stream));
+    launch_step(s);
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->host_ctl->fixed_dt = 0;
+    CUDA_TRY(cudaMemcpy(&s->ctl->fixed_dt, &s->host_ctl->fixed_dt, sizeof(double),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaGetLastError());
+    return SILT_OK;
+}
+
+int silt_solver_status(silt_solver* s, silt_status* st) {
+    if (!s || !st) return fail(SILT_ERR_INVALID, "silt_solver_status: null argument");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_status: call begin first");
+    Control* full = s->host_ctl;
+    Slot sl;
+    if (int rc = read_slot(s, &sl, full)) return rc;
+    st->t = sl.t;
+    st->steps = sl.steps;
+    st->state = sl.state;
+    st->last_dt = sl.last_dt;
+    st->snapshot_index = sl.snap_idx;
+    st->error_code = SILT_OK;
+    if (sl.err || sl.state == SILT_STATE_FAILED) {
+        st->state = SILT_STATE_FAILED;
+        const unsigned bits = sl.err ? sl.err : silt_dev::kErrDry;
+        st->error_code = error_from(*full, full->err_claim ? full->err_bits : bits);
+        return st->error_code;
+    }
+    return SILT_OK;
+}
+
+int silt_solver_resume(silt_solver* s) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    int st = 0;
+    Slot* slot = &s->ctl->slot[s->launches % 3];
+    CUDA_TRY(cudaMemcpy(&st, &slot->state, sizeof(int), cudaMemcpyDeviceToHost));
+    if (st == SILT_STATE_PAUSED) {
+        st = SILT_STATE_RUNNING;
+        CUDA_TRY(cudaMemcpy(&slot->state, &st, sizeof(int), cudaMemcpyHostToDevice));
+    }
+    return SILT_OK;
+}
+
+int silt_solver_dt_log(silt_solver* s, double* host_out, int64_t n) {
+    if (!s || (!host_out && n > 0)) return fail(SILT_ERR_INVALID, "silt_solver_dt_log: null");
+    if (n > s->dt_cap) return fail(SILT_ERR_INVALID, "silt_solver_dt_log: n exceeds capacity");
+    if (n == 0) return SILT_OK;
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    CUDA_TRY(cudaMemcpy(host_out, s->dt_log, n * sizeof(double), cudaMemcpyDeviceToHost));
+    return SILT_OK;
+}
+
+int silt_solver_cfl_dt(silt_solver* s, double* dt) {
+    if (!s || !dt) return fail(SILT_ERR_INVALID, "silt_solver_cfl_dt: null argument");
+    if (int rc = check_cfl(s->prob.cfl)) return rc;
+    if (!s->begun) {
+        silt_run_plan plan{INFINITY, -1, nullptr, 0, 0};
+        if (int rc = silt_solver_begin(s, &plan)) return rc;
+    }
+    Slot sl;
+    if (int rc = read_slot(s, &sl, nullptr)) return rc;
+    if (!sl.wet) return fail(SILT_ERR_INVALID, "cfl_dt: field is entirely dry");
+    double sx, sy;
+    std::memcpy(&sx, &sl.max_sx, sizeof(double));
+    std::memcpy(&sy, &sl.max_sy, sizeof(double));
+    double raw = s->args.dx / sx;
+    if (s->prob.dim == 2) raw = std::min(raw, s->args.dy / sy);
+    *dt = s->prob.cfl * raw;
+    return SILT_OK;
+}
+
+int silt_solver_reduce_slot(silt_solver* s, double** dev_ptr) {
+    if (!s || !dev_ptr) return fail(SILT_ERR_INVALID, "silt_solver_reduce_slot: null argument");
+    *dev_ptr = reinterpret_cast<double*>(&s->ctl->slot[s->launches % 3].max_sx);
+    return SILT_OK;
+}
+
+int silt_solver_exchange_ptrs(silt_solver* s, silt_exchange* out) {
+    if (!s || !out) return fail(SILT_ERR_INVALID, "silt_solver_exchange_ptrs: null argument");
+    out->send_south = s->strip.south_neighbor ? s->args.send_s : nullptr;
+    out->send_north = s->strip.north_neighbor ? s->args.send_n : nullptr;
+    out->recv_south = s->strip.south_neighbor ? s->args.recv_s : nullptr;
+    out->recv_north = s->strip.north_neighbor ? s->args.recv_n : nullptr;
+    out->row_doubles = 4 * (int64_t)s->nx;
+    return SILT_OK;
+}
+
+int silt_solver_launch_count(silt_solver* s, int64_t* count) {
+    if (!s || !count) return fail(SILT_ERR_INVALID, "null argument");
+    *count = s->kernel_count;
+    return SILT_OK;
+}
+
+// run_serial on the GPU (src/parallel.cpp:208-259)
+int silt_run(const silt_problem* problem, const double* init_aos, const silt_run_plan* plan,
+             int variant, double* out_aos, double* dt_log, int64_t dt_log_capacity,
+             silt_status* status) {
+    if (!plan || !init_aos || !out_aos) return fail(SILT_ERR_INVALID, "silt_run: null argument");
+    if (int rc = check_cfl(problem ? problem->cfl : 0.5)) return rc;
+    silt_solver* s = nullptr;
+    if (int rc = silt_solver_create(problem, nullptr, 0, variant, &s)) return rc;
+    silt_run_plan p = *plan;
+    p.dt_log_capacity = dt_log ? dt_log_capacity : 0;
+    int rc = silt_solver_upload(s, init_aos);
+    if (!rc) rc = silt_solver_begin(s, &p);
+    silt_status st{};
+    const int batch = 32;
+    while (!rc) {
+        rc = silt_solver_step(s, batch);
+        if (rc) break;
+        rc = silt_solver_status(s, &st);
+        if (rc) break;
+        if (st.state == SILT_STATE_PAUSED) {
+            rc = silt_solver_resume(s);
+            continue;
+        }
+        if (st.state == SILT_STATE_DONE) break;
+    }
+    if (!rc && dt_log) rc = silt_solver_dt_log(s, dt_log, std::min<int64_t>(st.steps, dt_log_capacity));
+    if (!rc) rc = silt_solver_download(s, out_aos);
+    if (status) *status = st;
+    const std::string keep = g_err;
+    silt_solver_destroy(s);
+    g_err = keep;
+    return rc;
+}
+
+int silt_cfl_dt(const silt_problem* problem, const double* field_aos, int variant, double* dt) {
+    if (int rc = check_cfl(problem ? problem->cfl : 0.5)) return rc;
+    silt_solver* s = nullptr;
+    if (int rc = silt_solver_create(problem, nullptr, 0, variant, &s)) return rc;
+    int rc = silt_solver_upload(s, field_aos);
+    if (!rc) rc = silt_solver_cfl_dt(s, dt);
+    const std::string keep = g_err;
+    silt_solver_destroy(s);
+    g_err = keep;
+    return rc;
+}
+
+// step_1d/step_2d on a halo-complete PaddedField (include/silt/stepper.hpp:47-54)
+int silt_step_padded(const silt_problem* problem, double* padded, double dt, int variant) {
+    if (!problem || !padded) return fail(SILT_ERR_INVALID, "silt_step_padded: null argument");
+    silt_problem p = *problem;
+    for (int k = 0; k < 4; ++k) p.bc[k].type = SILT_BC_GIVEN;
+    const int nx = p.nx, ny = p.dim == 1 ? 1 : p.ny;
+    const int W = nx + 2;
+    std::vector<double> interior(4 * (size_t)nx * ny), west(4 * (size_t)ny), east(4 * (size_t)ny),
+        south(4 * (size_t)nx), north(4 * (size_t)nx);
+    auto at = [&](int i, int j) { return padded + 4 * ((size_t)(j + 1) * W + (i + 1)); };
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) std::memcpy(&interior[4 * ((size_t)j * nx + i)], at(i, j), 32);
+    for (int j = 0; j < ny; ++j) {
+        std::memcpy(&west[4 * (size_t)j], at(-1, j), 32);
+        std::memcpy(&east[4 * (size_t)j], at(nx, j), 32);
+    }
+    for (int i = 0; i < nx; ++i) {
+        std::memcpy(&south[4 * (size_t)i], at(i, -1), 32);
+        std::memcpy(&north[4 * (size_t)i], at(i, ny), 32);
+    }
+    silt_solver* s = nullptr;
+    if (int rc = silt_solver_create(&p, nullptr, 0, variant, &s)) return rc;
+    int rc = silt_solver_upload(s, interior.data());
+    if (!rc) rc = silt_solver_set_ghosts(s, west.data(), east.data(), p.dim == 2 ? south.data() : nullptr,
+                                         p.dim == 2 ? north.data() : nullptr);
+    silt_run_plan plan{INFINITY, -1, nullptr, 0, 0};
+    if (!rc) rc = silt_solver_begin(s, &plan);
+    if (!rc) rc = silt_solver_step_fixed(s, dt);
+    silt_status st{};
+    if (!rc) rc = silt_solver_status(s, &st);
+    if (!rc) rc = silt_solver_download(s, interior.data());
+    if (!rc)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) std::memcpy(at(i, j), &interior[4 * ((size_t)j * nx + i)], 32);
+    const std::string keep = g_err;
+    silt_solver_destroy(s);
+    g_err = keep;
+    return rc;
+}
+
+int silt_riemann_batch(const silt_problem* problem, const double* left, const double* right,
+                       int64_t n, int axis, int variant, double* out) {
+    if (int rc = validate_problem(problem)) return rc;
+    if (n <= 0) return SILT_OK;
+    CUDA_TRY(cudaSetDevice(0));
+    silt_dev::Params P;
+    P.g = problem->gravity;
+    P.h_dry = problem->h_dry;
+    P.a_g = problem->a_g;
+    P.m_g = problem->m_g;
+    P.safety = problem->safety;
+    P.half_g = 0.5 * problem->gravity;
+    P.m3 = problem->m_g == 3.0;
+    double *dl = nullptr, *dr = nullptr, *dout = nullptr;
+    unsigned* derr = nullptr;
+    const size_t b4 = 4 * (size_t)n * sizeof(double), b5 = 5 * (size_t)n * sizeof(double);
+    CUDA_TRY(cudaMalloc(&dl, b4));
+    CUDA_TRY(cudaMalloc(&dr, b4));
+    CUDA_TRY(cudaMalloc(&dout, b5));
+    CUDA_TRY(cudaMalloc(&derr, sizeof(unsigned)));
+    cudaMemset(derr, 0, sizeof(unsigned));
+    cudaMemcpy(dl, left, b4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dr, right, b4, cudaMemcpyHostToDevice);
+    if (variant == SILT_VARIANT_STRICT)
+        silt_strict_faces(P, dl, dr, n, axis, dout, derr, 0);
+    else
+        silt_fast_faces(P, dl, dr, n, axis, dout, derr, 0);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned herr = 0;
+    cudaMemcpy(out, dout, b5, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&herr, derr, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    cudaFree(dl);
+    cudaFree(dr);
+    cudaFree(dout);
+    cudaFree(derr);
+    if (e != cudaSuccess) return fail(SILT_ERR_CUDA, cudaGetErrorString(e));
+    if (herr)
+        return fail(SILT_ERR_RUNTIME,
+                    "interface_riemann: no positive fan after 25 celerity enlargements");
+    return SILT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,563 @@
+// silt_kernels.cuh — the fused relaxation time step for sm_100a.
+//
+// Included by silt_fast.cu (S = false) and silt_strict.cu (S = true,
+// compiled with -fmad=false).  See DESIGN.md §Kernels for the roofline.
+//
+// K1 step2d: one launch per time step.  Each warp owns a column strip of 30
+// cells and marches up R rows.  Lane l holds column i0-1+l: lanes 1..30 own
+// cells, lanes 0 and 31 are the x-halo.  Per row:
+//   load state n (SoA, coalesced fp64) -> per-cell relaxation terms for the
+//   x and y axes (computed once, shared by both faces of the cell) ->
+//   x-face problem (right neighbour's terms by warp shuffle) -> x update ->
+//   y-face problem against the previous row (kept in registers) -> y update
+//   of the previous row -> check_depth -> store state n+1 -> CFL/hmax
+//   candidates of state n+1 (the NEXT step's cfl_dt) folded into registers.
+// Each face is solved exactly once per launch (faces on strip seams by the
+// warp to their left... no: the x-halo lanes make every face belong to
+// exactly one warp), so depth and bed updates telescope exactly.
+//
+// The run clock lives on the device (Control, triple-buffered per launch):
+// every CTA derives dt_n from the previous launch's reduced axis speeds and
+// the clipping rule of run_serial (src/parallel.cpp:221-237), so a batch of
+// steps needs no host round trip.
+#pragma once
+#include "silt_layout.h"
+#include "silt_physics.cuh"
+
+namespace silt_dev {
+
+__device__ __forceinline__ double shfl_down_d(double v, int d) {
+    return __shfl_down_sync(0xffffffffu, v, d);
+}
+__device__ __forceinline__ double shfl_up_d(double v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+__device__ __forceinline__ Side shfl_down_side(const Side& s) {
+    Side o;
+    o.h = shfl_down_d(s.h, 1);
+    o.hun = shfl_down_d(s.hun, 1);
+    o.pi = shfl_down_d(s.pi, 1);
+    o.z = shfl_down_d(s.z, 1);
+    o.omega = shfl_down_d(s.omega, 1);
+    o.un = shfl_down_d(s.un, 1);
+    o.ut = shfl_down_d(s.ut, 1);
+    o.tau = shfl_down_d(s.tau, 1);
+    o.a_side = shfl_down_d(s.a_side, 1);
+    o.b2_side = shfl_down_d(s.b2_side, 1);
+    const int packed = __shfl_down_sync(0xffffffffu, s.wet | (s.moving << 1), 1);
+    o.wet = packed & 1;
+    o.moving = (packed >> 1) & 1;
+    return o;
+}
+
+// ---- control block --------------------------------------------------------
+struct RunDecision {
+    bool run;
+    double dt, t_new;
+    int next_state;
+    int snap_idx;
+    bool landed;
+};
+
+// Mirrors one trip of run_serial's loop head (src/parallel.cpp:221-237):
+// loop condition, cfl_dt from the reduced speeds (src/stepper.cpp:38-58:
+// min over cells of dx/s == dx / max s since RN division is monotone), clip
+// to the next stop (next_stop, :129-132).
+__device__ __forceinline__ RunDecision decide(const StepArgs& A, const Slot& cur) {
+    const Control& C = *A.ctl;
+    RunDecision d;
+    d.run = false;
+    d.dt = 0;
+    d.t_new = cur.t;
+    d.snap_idx = cur.snap_idx;
+    d.landed = false;
+    d.next_state = cur.state;
+    if (cur.state != SILT_STATE_RUNNING) return d;
+    if (cur.err) {
+        d.next_state = SILT_STATE_FAILED;
+        return d;
+    }
+    if (C.fixed_dt > 0) {
+        d.run = true;
+        d.dt = C.fixed_dt;
+        d.t_new = cur.t + d.dt;
+        return d;
+    }
+    if (!(cur.t < C.t_end && (C.max_steps < 0 || cur.steps < C.max_steps))) {
+        d.next_state = SILT_STATE_DONE;
+        return d;
+    }
+    if (!cur.wet) {
+        d.next_state = SILT_STATE_FAILED;
+        return d;
+    }
+    const double sx = __longlong_as_double((long long)cur.max_sx);
+    const double sy = __longlong_as_double((long long)cur.max_sy);
+    double raw = A.dx / sx;
+    if (A.dim == 2) raw = smin(raw, A.dy / sy);
+    raw = A.cfl * raw;
+    const double stop = (cur.snap_idx < C.n_snaps) ? smin(C.snaps[cur.snap_idx], C.t_end) : C.t_end;
+    if (stop - cur.t <= raw) {
+        d.dt = stop - cur.t;
+        d.t_new = stop;
+    } else {
+        d.dt = raw;
+        d.t_new = cur.t + d.dt;
+    }
+    d.run = true;
+    if (cur.snap_idx < C.n_snaps && d.t_new == C.snaps[cur.snap_idx]) {
+        d.landed = true;
+        d.snap_idx = cur.snap_idx + 1;
+        d.next_state = SILT_STATE_PAUSED;
+    }
+    return d;
+}
+
+// Block (0,0) thread 0: publish the next header, clear the slot after next.
+__device__ __forceinline__ void control_epilogue(const StepArgs& A, int li, const Slot& cur,
+                                                 const RunDecision& d) {
+    Control& C = *A.ctl;
+    Slot& nxt = C.slot[(li + 1) % 3];
+    Slot& clr = C.slot[(li + 2) % 3];
+    clr.max_sx = clr.max_sy = clr.hmax = 0ull;
+    clr.wet = 0u;
+    clr.err = 0u;
+    if (d.run) {
+        nxt.t = d.t_new;
+        nxt.steps = cur.steps + 1;
+        nxt.last_dt = d.dt;
+        nxt.snap_idx = d.snap_idx;
+        nxt.state = d.next_state;
+        if (C.fixed_dt <= 0 && C.dt_log && cur.steps < C.dt_cap) C.dt_log[cur.steps] = d.dt;
+    } else {
+        nxt.t = cur.t;
+        nxt.steps = cur.steps;
+        nxt.last_dt = cur.last_dt;
+        nxt.snap_idx = cur.snap_idx;
+        nxt.state = d.next_state;
+        nxt.max_sx = cur.max_sx;
+        nxt.max_sy = cur.max_sy;
+        nxt.hmax = cur.hmax;
+        nxt.wet = cur.wet;
+        nxt.err = cur.err | ((d.next_state == SILT_STATE_FAILED && !cur.err) ? kErrDry : 0u);
+    }
+}
+
+__device__ __forceinline__ void record_error(const StepArgs& A, unsigned bit, int col, int row,
+                                             const double* info6, Slot& nxt) {
+    atomicOr(&nxt.err, bit);
+    if (atomicCAS(&A.ctl->err_claim, 0u, 1u) == 0u) {
+        A.ctl->err_bits = bit;
+        A.ctl->err_col = col;
+        A.ctl->err_row = row;
+        for (int k = 0; k < 6; ++k) A.ctl->err_info[k] = info6 ? info6[k] : 0.0;
+    }
+}
+
+// ---- cell access ----------------------------------------------------------
+// Ghost value for a physical side (ghost_value, src/scenarios.cpp:43-74).
+__device__ __forceinline__ void ghost_transform(const StepArgs& A, int side, double c[4]) {
+    const int t = A.bc_type[side];
+    const bool xside = side == SILT_WEST || side == SILT_EAST;
+    if (t == SILT_BC_INFLOW) {
+        if (A.bc_super[side]) c[0] = A.bc_h0[side];
+        if (xside) {
+            c[1] = A.bc_q0[side];
+            c[2] = 0.0;
+        } else {
+            c[2] = A.bc_q0[side];
+            c[1] = 0.0;
+        }
+    } else if (t == SILT_BC_WALL) {
+        if (xside)
+            c[1] = -c[1];
+        else
+            c[2] = -c[2];
+    }
+}
+
+__device__ __forceinline__ void load_interior(const StepArgs& A, int p, int col, int row,
+                                              double c[4]) {
+    const size_t off = (size_t)row * A.pitch + col;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) c[f] = __ldg(A.state[p][f] + off);
+}
+
+// Cell (col, row) of state parity p, ghosts synthesised: rows -1 / ny come
+// from the ghost-row buffers (BC rows written by the previous launch, or rows
+// received from a neighbour strip); columns -1 / nx are built from the x-side
+// boundary condition (apply_bc_side, src/scenarios.cpp:78-99) or wrap
+// (periodic), or come from caller-supplied ghost columns (GIVEN).
+__device__ __forceinline__ void load_cell(const StepArgs& A, int p, int col, int row, double c[4]) {
+    const int nx = A.nx;
+    if (row < 0 || row >= A.ny) {
+        const double* g;
+        if (row < 0)
+            g = A.south_nbr ? A.recv_s : A.ghost_s[p];
+        else
+            g = A.north_nbr ? A.recv_n : A.ghost_n[p];
+        const int cc = min(max(col, 0), nx - 1);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) c[f] = g[(size_t)f * nx + cc];
+        return;
+    }
+    if (col >= 0 && col < nx) {
+        load_interior(A, p, col, row, c);
+        return;
+    }
+    if (col < -1 || col > nx) {  // dead lane: any valid cell
+        load_interior(A, p, col < 0 ? 0 : nx - 1, row, c);
+        return;
+    }
+    const int side = col < 0 ? SILT_WEST : SILT_EAST;
+    const int t = A.bc_type[side];
+    if (t == SILT_BC_PERIODIC) {
+        load_interior(A, p, col < 0 ? nx - 1 : 0, row, c);
+        return;
+    }
+    if (t == SILT_BC_GIVEN) {
+        const double* g = side == SILT_WEST ? A.ghost_w : A.ghost_e;
+#pragma unroll
+        for (int f = 0; f < 4; ++f) c[f] = g[(size_t)f * A.ny + row];
+        return;
+    }
+    load_interior(A, p, col < 0 ? 0 : nx - 1, row, c);
+    ghost_transform(A, side, c);
+}
+
+// Ghost rows of a freshly written edge row (row 0 or ny-1) for the next
+// state parity q: physical BC ghost, periodic self-wrap, or the send buffer
+// for a neighbour strip.
+__device__ __forceinline__ void write_edges(const StepArgs& A, int q, int col, int row,
+                                            const double c[4]) {
+    if (row == 0) {
+        if (A.south_nbr) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.send_s[(size_t)f * A.nx + col] = c[f];
+        } else if (A.per_y_self) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.ghost_n[q][(size_t)f * A.nx + col] = c[f];
+        } else if (A.bc_type[SILT_SOUTH] != SILT_BC_GIVEN) {
+            double g[4] = {c[0], c[1], c[2], c[3]};
+            ghost_transform(A, SILT_SOUTH, g);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.ghost_s[q][(size_t)f * A.nx + col] = g[f];
+        }
+    }
+    if (row == A.ny - 1) {
+        if (A.north_nbr) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.send_n[(size_t)f * A.nx + col] = c[f];
+        } else if (A.per_y_self) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.ghost_s[q][(size_t)f * A.nx + col] = c[f];
+        } else if (A.bc_type[SILT_NORTH] != SILT_BC_GIVEN) {
+            double g[4] = {c[0], c[1], c[2], c[3]};
+            ghost_transform(A, SILT_NORTH, g);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.ghost_n[q][(size_t)f * A.nx + col] = g[f];
+        }
+    }
+}
+
+// Per-cell CFL candidates of a state (axis_speed, src/stepper.cpp:30-36, on
+// primitives of a wet cell).
+template <bool S>
+__device__ __forceinline__ void cell_speeds(const StepArgs& A, const double c[4], double& sx,
+                                            double& sy) {
+    const Params& P = A.P;
+    const double h = c[0];
+    if constexpr (S) {
+        const double u = c[1] / h, v = c[2] / h;
+        sx = axis_speed_ref(P, h, u, v);
+        sy = (A.dim == 2) ? axis_speed_ref(P, h, v, u) : 0.0;
+    } else {
+        const double rh = rcp(h);
+        const double u = c[1] * rh, v = c[2] * rh;
+        const double gh = P.g * h;
+        const double s2 = fma(u, u, v * v);
+        double dqx = 0, dqy = 0, om;
+        grass_terms_fast(P, u, v, s2, om, dqx);
+        const double au = fabs(u), av = fabs(v);
+        sx = au + sqrt(smax(gh, fma(u, u, P.g * dqx)));
+        if (A.dim == 2) {
+            grass_terms_fast(P, v, u, s2, om, dqy);
+            sy = av + sqrt(smax(gh, fma(v, v, P.g * dqy)));
+        } else {
+            sy = 0.0;
+        }
+    }
+}
+
+struct Reduce {
+    double sx, sy, hmax;
+    unsigned wet;
+};
+
+__device__ __forceinline__ void reduce_fold(const StepArgs& A, Reduce& R, const double c[4],
+                                            double sx, double sy) {
+    R.hmax = smax(R.hmax, c[0]);
+    if (c[0] > A.P.h_dry) {
+        R.wet = 1u;
+        if (sx == sx) R.sx = smax(R.sx, sx);
+        if (sy == sy) R.sy = smax(R.sy, sy);
+    }
+}
+
+// warp reduce + one conditional atomic per warp into the slot
+__device__ __forceinline__ void reduce_flush(Reduce R, Slot& s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        R.sx = smax(R.sx, __shfl_xor_sync(0xffffffffu, R.sx, o));
+        R.sy = smax(R.sy, __shfl_xor_sync(0xffffffffu, R.sy, o));
+        R.hmax = smax(R.hmax, __shfl_xor_sync(0xffffffffu, R.hmax, o));
+        R.wet |= __shfl_xor_sync(0xffffffffu, R.wet, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        volatile Slot& vs = s;
+        if (R.sx > 0 && R.sx > __longlong_as_double((long long)vs.max_sx))
+            atomicMax(&s.max_sx, (unsigned long long)__double_as_longlong(R.sx));
+        if (R.sy > 0 && R.sy > __longlong_as_double((long long)vs.max_sy))
+            atomicMax(&s.max_sy, (unsigned long long)__double_as_longlong(R.sy));
+        if (R.hmax > 0 && R.hmax > __longlong_as_double((long long)vs.hmax))
+            atomicMax(&s.hmax, (unsigned long long)__double_as_longlong(R.hmax));
+        if (R.wet && !vs.wet) atomicOr(&s.wet, 1u);
+    }
+}
+
+template <bool S>
+__device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4], Side& sx, Side& sy,
+                                           bool need_x) {
+    if constexpr (S) {
+        if (need_x) sx = make_side_ref(A.P, c[0], c[1], c[2], c[3]);
+        sy = make_side_ref(A.P, c[0], c[2], c[1], c[3]);
+    } else {
+        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
+        if (need_x) sx = make_side_fast(A.P, pre, true);
+        sy = make_side_fast(A.P, pre, false);
+    }
+}
+
+// ---- K1: fused 2D step ----------------------------------------------------
+template <bool S>
+__global__ void __launch_bounds__(kStepThreads) step2d_kernel(StepArgs A, int li) {
+    const Slot cur = A.ctl->slot[li % 3];
+    const RunDecision d = decide(A, cur);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) control_epilogue(A, li, cur, d);
+    if (!d.run) return;
+    Slot& nxt = A.ctl->slot[(li + 1) % 3];
+
+    const int p = (int)(cur.steps & 1), q = p ^ 1;
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * (kStepThreads / 32) + (threadIdx.x >> 5);
+    const int i0 = strip * kCellsPerWarp;
+    if (i0 >= A.nx) return;  // warp-uniform
+    const int col = i0 - 1 + lane;
+    const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < A.nx;
+    const bool xface = lane <= kCellsPerWarp && col <= A.nx - 1;  // face at right of col
+    const int jb = blockIdx.y * A.rows_per_block;
+    const int je = min(jb + A.rows_per_block, A.ny);
+    if (jb >= je) return;
+    const double cx = d.dt / A.dx;
+    const double cy = d.dt / A.dy;
+    const double href = __longlong_as_double((long long)cur.hmax);
+
+    Reduce R{0.0, 0.0, 0.0, 0u};
+    Side yprev;
+    double xs_prev[4] = {0, 0, 0, 0};
+    Flux fy_prev{0, 0, 0, 0, 0};
+    bool fail_riemann = false;
+
+    double c[4];
+    load_cell(A, p, col, jb - 1, c);
+    for (int r = jb - 1; r <= je; ++r) {
+        double cn[4];
+        if (r < je) load_cell(A, p, col, r + 1, cn);  // prefetch next row
+        const bool own_row = r >= jb && r < je;
+        Side sx, sy;
+        make_sides<S>(A, c, sx, sy, own_row);
+        double xs[4] = {c[0], c[1], c[2], c[3]};
+        if (own_row) {
+            // x faces: this lane solves the face between col and col+1
+            const Side right = shfl_down_side(sx);
+            Flux fx{0, 0, 0, 0, 0};
+            if (xface) {
+                if (!face_flux<S>(A.P, sx, right, fx)) {
+                    const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
+                    record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
+                    fail_riemann = true;
+                }
+            }
+            const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
+            const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
+            // x update (step_2d x sweep, src/stepper.cpp:165-170)
+            xs[0] = c[0] - cx * (fx.h - lh);
+            xs[1] = c[1] - cx * (fx.huL - lhuR);
+            xs[2] = c[2] - cx * (fx.hv - lhv);
+            xs[3] = c[3] - cx * (fx.z - lz);
+        }
+        if (r > jb - 1) {
+            // y face between rows r-1 and r (normal = v, transverse = u)
+            Flux fy{0, 0, 0, 0, 0};
+            if (owned) {
+                if (!face_flux<S>(A.P, yprev, sy, fy)) {
+                    const double info[6] = {yprev.h, yprev.un, yprev.z, sy.h, sy.un, sy.z};
+                    record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
+                    fail_riemann = true;
+                }
+            }
+            if (r - 1 >= jb && owned) {
+                // y update of row r-1 (src/stepper.cpp:181-186) + check_depth
+                double o[4];
+                o[0] = xs_prev[0] - cy * (fy.h - fy_prev.h);
+                o[2] = xs_prev[2] - cy * (fy.huL - fy_prev.huR);
+                o[1] = xs_prev[1] - cy * (fy.hv - fy_prev.hv);
+                o[3] = xs_prev[3] - cy * (fy.z - fy_prev.z);
+                if (!check_depth(o[0], href)) {
+                    record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
+                }
+                const size_t off = (size_t)(r - 1) * A.pitch + col;
+#pragma unroll
+                for (int f = 0; f < 4; ++f) A.state[q][f][off] = o[f];
+                write_edges(A, q, col, r - 1, o);
+                double ssx, ssy;
+                cell_speeds<S>(A, o, ssx, ssy);
+                reduce_fold(A, R, o, ssx, ssy);
+            }
+            fy_prev = fy;
+        }
+        yprev = sy;
+#pragma unroll
+        for (int f = 0; f < 4; ++f) xs_prev[f] = xs[f];
+        if (r < je) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) c[f] = cn[f];
+        }
+    }
+    (void)fail_riemann;
+    reduce_flush(R, nxt);
+}
+
+// ---- K2: 1D step (step_1d, src/stepper.cpp:118-140) ----------------------
+template <bool S>
+__global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li) {
+    const Slot cur = A.ctl->slot[li % 3];
+    const RunDecision d = decide(A, cur);
+    if (blockIdx.x == 0 && threadIdx.x == 0) control_epilogue(A, li, cur, d);
+    if (!d.run) return;
+    Slot& nxt = A.ctl->slot[(li + 1) % 3];
+    const int p = (int)(cur.steps & 1), q = p ^ 1;
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * (kStepThreads / 32) + (threadIdx.x >> 5);
+    const int i0 = strip * kCellsPerWarp;
+    if (i0 >= A.nx) return;
+    const int col = i0 - 1 + lane;
+    const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < A.nx;
+    const bool xface = lane <= kCellsPerWarp && col <= A.nx - 1;
+    const double c1 = d.dt / A.dx;
+    const double href = __longlong_as_double((long long)cur.hmax);
+    double c[4];
+    load_cell(A, p, col, 0, c);
+    Side sx;
+    if constexpr (S) {
+        sx = make_side_ref(A.P, c[0], c[1], c[2], c[3]);
+    } else {
+        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
+        sx = make_side_fast(A.P, pre, true);
+    }
+    const Side right = shfl_down_side(sx);
+    Flux fx{0, 0, 0, 0, 0};
+    if (xface && !face_flux<S>(A.P, sx, right, fx)) {
+        const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
+        record_error(A, kErrRiemann, col, 0, info, nxt);
+    }
+    const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
+    const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
+    Reduce R{0.0, 0.0, 0.0, 0u};
+    if (owned) {
+        double o[4];
+        o[0] = c[0] - c1 * (fx.h - lh);
+        o[1] = c[1] - c1 * (fx.huL - lhuR);
+        o[2] = c[2] - c1 * (fx.hv - lhv);
+        o[3] = c[3] - c1 * (fx.z - lz);
+        if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, 0, nullptr, nxt);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) A.state[q][f][col] = o[f];
+        double ssx, ssy;
+        cell_speeds<S>(A, o, ssx, ssy);
+        reduce_fold(A, R, o, ssx, ssy);
+    }
+    reduce_flush(R, nxt);
+}
+
+// ---- initial reduction of a state (first cfl_dt + hmax + ghost rows) --------
+template <bool S>
+__global__ void __launch_bounds__(256) reduce_state_kernel(StepArgs A, int li) {
+    Slot& s = A.ctl->slot[li % 3];
+    const int p = (int)(s.steps & 1);
+    Reduce R{0.0, 0.0, 0.0, 0u};
+    const long long n = (long long)A.nx * A.ny;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(k / A.nx), col = (int)(k % A.nx);
+        double c[4];
+        load_interior(A, p, col, row, c);
+        if (A.write_edges_in_reduce) write_edges(A, p, col, row, c);
+        double sx = 0, sy = 0;
+        if (c[0] > A.P.h_dry) cell_speeds<S>(A, c, sx, sy);
+        reduce_fold(A, R, c, sx, sy);
+    }
+    reduce_flush(R, s);
+}
+
+// ---- batch of interface problems (unit tests / ABI silt_riemann_batch) -------
+template <bool S>
+__global__ void face_batch_kernel(Params P, const double* L, const double* Rr, long long n,
+                                  int axis, double* out, unsigned* err) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double l[4], r[4];
+    for (int f = 0; f < 4; ++f) {
+        l[f] = L[4 * k + f];
+        r[f] = Rr[4 * k + f];
+    }
+    Side sl, sr;
+    const int nn = axis == 0 ? 1 : 2, tt = axis == 0 ? 2 : 1;
+    if constexpr (S) {
+        sl = make_side_ref(P, l[0], l[nn], l[tt], l[3]);
+        sr = make_side_ref(P, r[0], r[nn], r[tt], r[3]);
+    } else {
+        const CellPre pl = cell_pre_fast(P, l[0], l[1], l[2], l[3]);
+        const CellPre pr = cell_pre_fast(P, r[0], r[1], r[2], r[3]);
+        sl = make_side_fast(P, pl, axis == 0);
+        sr = make_side_fast(P, pr, axis == 0);
+    }
+    Flux F;
+    if (!face_flux<S>(P, sl, sr, F)) atomicOr(err, kErrRiemann);
+    out[5 * k + 0] = F.h;
+    out[5 * k + 1] = F.huL;
+    out[5 * k + 2] = F.huR;
+    out[5 * k + 3] = F.hv;
+    out[5 * k + 4] = F.z;
+}
+
+}  // namespace silt_dev
+
+// Explicit instantiation hooks, defined by each TU with its own S.
+#define SILT_DEFINE_LAUNCHERS(S, NAME)                                                          \
+    void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st) {                    \
+        if (A.dim == 2)                                                                          \
+            silt_dev::step2d_kernel<S><<<grid, kStepThreads, 0, st>>>(A, li);                    \
+        else                                                                                     \
+            silt_dev::step1d_kernel<S><<<grid, kStepThreads, 0, st>>>(A, li);                    \
+    }                                                                                            \
+    void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st) {                 \
+        silt_dev::reduce_state_kernel<S><<<blocks, 256, 0, st>>>(A, li);                         \
+    }                                                                                            \
+    void NAME##_faces(const silt_dev::Params& P, const double* L, const double* R, long long n,  \
+                      int axis, double* out, unsigned* err, cudaStream_t st) {                   \
+        const int b = 128;                                                                       \
+        silt_dev::face_batch_kernel<S><<<(unsigned)((n + b - 1) / b), b, 0, st>>>(P, L, R, n,    \
+                                                                                  axis, out,     \
+                                                                                  err);          \
+    }

@@ -1,0 +1,14 @@
+// silt_launch.h — launchers exported by the two numerical-variant TUs.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "silt_layout.h"
+
+#define SILT_DECLARE_LAUNCHERS(NAME)                                                         \
+    void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st);                 \
+    void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st);              \
+    void NAME##_faces(const silt_dev::Params& P, const double* L, const double* R,           \
+                      long long n, int axis, double* out, unsigned* err, cudaStream_t st);
+
+SILT_DECLARE_LAUNCHERS(silt_fast)
+SILT_DECLARE_LAUNCHERS(silt_strict)

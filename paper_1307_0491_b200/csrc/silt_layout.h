@@ -1,0 +1,77 @@
+// silt_layout.h — device data layout shared by the host runtime and kernels.
+//
+// HBM layout of one strip:
+//   state[2][4]  : ping-pong SoA planes h, hu, hv, zb, each [ny][pitch] fp64,
+//                  pitch = nx rounded up to 32 doubles (256 B rows)
+//   ghost_s/n[2] : ghost rows -1 / ny per parity, [4][nx] (physical BC rows,
+//                  periodic self-wrap or caller-given rows)
+//   recv_s/n     : ghost rows received from neighbour strips, [4][nx]
+//   send_s/n     : edge rows 0 / ny-1 for neighbour strips, [4][nx]
+//   ghost_w/e    : caller-given ghost columns (SILT_BC_GIVEN), [4][ny]
+//   Control      : triple-buffered run-clock/reduction mailboxes
+#pragma once
+#include <stdint.h>
+
+#include "silt_cuda.h"
+#include "silt_physics_params.h"
+
+constexpr int kStepThreads = 128;   // 4 warps per CTA, one column strip each
+constexpr int kCellsPerWarp = 30;   // lanes 1..30 own cells, 0/31 are x-halo
+
+// One mailbox per launch index mod 3.  Launch n reads slot[n%3] (state n's
+// reduced speeds + run clock), accumulates state n+1 into slot[(n+1)%3] and
+// clears slot[(n+2)%3].  max_* hold the bits of non-negative doubles so that
+// integer atomicMax orders them like the values.
+struct Slot {
+    unsigned long long max_sx;  // max over wet cells of the x axis speed
+    unsigned long long max_sy;  // (adjacent: a multi-rank driver all-reduces
+                                //  these two as float64 MAX)
+    unsigned long long hmax;    // max depth of the strip (check_depth href)
+    unsigned int wet;           // strip has a wet cell
+    unsigned int err;           // error bits raised producing this state
+    double t;                   // simulated time of this state
+    double last_dt;
+    long long steps;            // steps taken to reach this state
+    int snap_idx;
+    int state;                  // SILT_STATE_*
+};
+
+struct Control {
+    Slot slot[3];
+    double t_end;
+    double fixed_dt;      // > 0: step_1d/step_2d with a caller dt
+    long long max_steps;
+    long long dt_cap;
+    double* dt_log;
+    const double* snaps;
+    int n_snaps;
+    unsigned int err_claim;
+    unsigned int err_bits;
+    int err_col, err_row;
+    int pad_;
+    double err_info[6];
+};
+
+struct StepArgs {
+    int dim, nx, ny, pitch;
+    int j0;                 // global row of local row 0 (messages)
+    int rows_per_block;
+    int south_nbr, north_nbr, per_y_self;
+    int write_edges_in_reduce;
+    double dx, dy, cfl;
+    silt_dev::Params P;
+    int bc_type[4];
+    int bc_super[4];
+    double bc_q0[4];
+    double bc_h0[4];
+    double* state[2][4];
+    double* ghost_s[2];
+    double* ghost_n[2];
+    double* recv_s;
+    double* recv_n;
+    double* send_s;
+    double* send_n;
+    double* ghost_w;
+    double* ghost_e;
+    Control* ctl;
+};

@@ -1,0 +1,620 @@
+// silt_physics.cuh — device math of the relaxation time step (sm_100a).
+//
+// One source, two numerical variants selected by the template flag S:
+//   S = true  (STRICT): the reference's operation order, IEEE division/sqrt,
+//                       glibc's hypot algorithm; the including TU is compiled
+//                       with -fmad=false, so results are bit-identical to the
+//                       CPU reference (proj/core/src, built -O3 without FMA).
+//   S = false (FAST):   the same algorithm with reciprocal reuse, per-cell
+//                       common-subexpression sharing, closed-form Grass terms
+//                       for m_g = 3 and FMA contraction.  Parity bar: 1e-9
+//                       normwise (BASELINE.json north_star).
+//
+// Citations are paths under the reference checkout proj/core/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "silt_physics_params.h"
+
+namespace silt_dev {
+
+// ---- constants (src/bedload.cpp:11, src/riemann.cpp:42-45) --------------
+constexpr double kUEps = 1e-10;
+constexpr double kSuppressB = 1e-12;
+constexpr double kGap = 1.1;
+constexpr int kMaxEnlarge = 25;
+constexpr int kMaxNewton = 60;
+
+
+// std::max / std::min semantics (first argument kept on ties / NaN in b)
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+// Round-to-nearest reciprocal (MUFU.RCP64H + Newton, IEEE-rounded).
+__device__ __forceinline__ double rcp(double y) { return __drcp_rn(y); }
+
+// glibc 2.39 hypot (sysdeps/ieee754/dbl-64/e_hypot.c, non-FMA kernel after
+// C. F. Borges, "An improved algorithm for hypot(a,b)", 2019), restated so the
+// STRICT variant reproduces the reference's libm hypot bit for bit (verified
+// on 2e7 random pairs).  Scaling branches for |x| > 2^511 or
+// |y| < 2^-511 are included for completeness.
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+    double t1, t2;
+    double h = sqrt(ax * ax + ay * ay);
+    if (h <= 2.0 * ay) {
+        const double delta = h - ay;
+        t1 = ax * (2.0 * delta - ax);
+        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    } else {
+        const double delta = h - ax;
+        t1 = 2.0 * delta * (ax - 2.0 * ay);
+        t2 = (4.0 * delta - ay) * ay + delta * delta;
+    }
+    h -= (t1 + t2) / (2.0 * h);
+    return h;
+}
+
+static __device__ __noinline__ double hypot_glibc(double x, double y) {
+    if (!isfinite(x) || !isfinite(y)) {
+        if (isinf(x) || isinf(y)) return __longlong_as_double(0x7ff0000000000000ll);
+        return x + y;
+    }
+    x = fabs(x);
+    y = fabs(y);
+    double ax = x < y ? y : x;
+    double ay = x < y ? x : y;
+    const double kScale = 0x1p-600, kEps = 0x1p-54;
+    if (ax > 0x1p+511) {
+        if (ay <= ax * kEps) return ax + ay;
+        return hypot_kernel(ax * kScale, ay * kScale) / kScale;
+    }
+    if (ay < 0x1p-511) {
+        if (ax >= ay / kEps) return ax + ay;
+        return hypot_kernel(ax / kScale, ay / kScale) * kScale;
+    }
+    if (ay <= ax * kEps) return ax + ay;
+    return hypot_kernel(ax, ay);
+}
+
+// abs_pow: src/bedload.cpp:14-20
+__device__ __forceinline__ double abs_pow(double au, double p) {
+    if (p == 0.0) return 1.0;
+    if (p == 1.0) return au;
+    if (p == 2.0) return au * au;
+    if (p == 3.0) return au * au * au;
+    return pow(au, p);
+}
+
+// grass_flux: src/bedload.cpp:78-80
+__device__ __forceinline__ double grass_flux(double u, double a_g, double m_g) {
+    return a_g * u * abs_pow(fabs(u), m_g - 1.0);
+}
+
+// normal_flux: src/bedload.cpp:207-213 (STRICT)
+__device__ __forceinline__ double normal_flux_ref(const Params& P, double un, double ut) {
+    const double speed = hypot_glibc(un, ut);
+    if (speed <= kUEps) return 0.0;
+    return grass_flux(speed, P.a_g, P.m_g) * (un / speed);
+}
+
+// normal_flux_derivative: src/bedload.cpp:215-223 (STRICT); flux_derivatives
+// Grass branch :165-177 inlined.
+__device__ __forceinline__ double normal_flux_derivative_ref(const Params& P, double h,
+                                                             double un, double ut) {
+    const double speed = hypot_glibc(un, ut);
+    if (speed <= kUEps) return 0.0;
+    const double rate = grass_flux(speed, P.a_g, P.m_g);
+    double drate = 0.0;
+    const double hu = h * speed;
+    if (h > 0) {
+        const double u = hu / h;
+        drate = P.a_g * P.m_g * abs_pow(fabs(u), P.m_g - 1.0);
+    }
+    const double ratio = un / speed;
+    return rate / speed + ratio * ratio * (drate - rate / speed);
+}
+
+// Grass rate, its planar normal component and u_n-derivative from the squared
+// speed (FAST).  Same cut-offs as the reference (speed <= kUEps -> 0).
+__device__ __forceinline__ void grass_terms_fast(const Params& P, double un, double ut,
+                                                 double s2, double& omega, double& dq) {
+    if (!(s2 > kUEps * kUEps)) {
+        omega = 0.0;
+        dq = 0.0;
+        return;
+    }
+    if (P.m3) {  // q = a s^3: omega = a s^2 u_n, dq = a (3 u_n^2 + u_t^2)
+        omega = P.a_g * s2 * un;
+        dq = P.a_g * fma(3.0 * un, un, ut * ut);
+        return;
+    }
+    const double s = sqrt(s2);
+    const double is = rcp(s);
+    const double rate = grass_flux(s, P.a_g, P.m_g);
+    const double drate = P.a_g * P.m_g * abs_pow(s, P.m_g - 1.0);
+    const double ratio = un * is;
+    omega = rate * ratio;
+    dq = rate * is + ratio * ratio * (drate - rate * is);
+}
+
+// ---- one cell seen from one face axis ------------------------------------
+// RelaxState (include/silt/relax_state.hpp:14-22) plus the per-side pieces of
+// bounds_impl (src/relax_state.cpp:25-53) and of the Riemann solver that only
+// depend on this cell.  Computed once per cell and axis, shared by both faces.
+struct Side {
+    double h, hun, pi, z, omega;  // RelaxState
+    double un;                    // RelaxState::u(h_dry) == u(0.0)
+    double ut;                    // transverse primitive velocity
+    double tau;                   // 1 / max(h, 1e-12)   (src/riemann.cpp:50-52)
+    double a_side;                // h sqrt(g h) if wet else 0
+    double b2_side;               // (h u_n)^2 + g h^2 dq/du_n if wet else 0
+    int wet, moving;
+};
+
+// STRICT side: equilibrate (src/relax_state.cpp:8-21) with primitives
+// (src/grid.cpp:47-59), then the side terms of bounds_impl exactly as written.
+__device__ __forceinline__ Side make_side_ref(const Params& P, double h, double hu_n,
+                                              double hu_t, double zb) {
+    Side s;
+    const bool wet = h > P.h_dry;
+    const double un_p = wet ? hu_n / h : 0.0;
+    const double ut_p = wet ? hu_t / h : 0.0;
+    s.h = h;
+    s.hun = h * un_p;
+    s.pi = 0.5 * P.g * h * h;
+    s.z = zb;
+    s.omega = normal_flux_ref(P, un_p, ut_p);
+    s.ut = ut_p;
+    s.wet = wet;
+    s.un = wet ? s.hun / h : 0.0;
+    s.tau = 1.0 / smax(h, 1e-12);
+    if (wet) {
+        s.a_side = h * sqrt(P.g * h);
+        const double dq = normal_flux_derivative_ref(P, h, s.un, ut_p);
+        s.b2_side = s.hun * s.hun + P.g * h * h * dq;
+        const double speed = hypot_glibc(s.un, ut_p);
+        s.moving = (grass_flux(speed, P.a_g, P.m_g) != 0.0 || dq != 0.0 || s.omega != 0.0);
+    } else {
+        s.a_side = 0.0;
+        s.b2_side = 0.0;
+        s.moving = 0;
+    }
+    return s;
+}
+
+// Per-cell quantities shared by both axes (FAST).
+struct CellPre {
+    double h, hu, hv, zb;
+    double u, v, s2, pi, tau, sq;  // sq = sqrt(g h)
+    int wet;
+};
+
+__device__ __forceinline__ CellPre cell_pre_fast(const Params& P, double h, double hu, double hv,
+                                                 double zb) {
+    CellPre c;
+    c.h = h;
+    c.hu = hu;
+    c.hv = hv;
+    c.zb = zb;
+    c.wet = h > P.h_dry;
+    const double rh = rcp(h);
+    c.u = c.wet ? hu * rh : 0.0;
+    c.v = c.wet ? hv * rh : 0.0;
+    c.s2 = fma(c.u, c.u, c.v * c.v);
+    c.pi = P.half_g * h * h;
+    c.tau = (h >= 1e-12) ? rh : 1e12;
+    c.sq = c.wet ? sqrt(P.g * h) : 0.0;
+    return c;
+}
+
+// FAST side for axis X (xaxis=1: normal u) or Y (normal v).
+__device__ __forceinline__ Side make_side_fast(const Params& P, const CellPre& c, bool xaxis) {
+    Side s;
+    const double un = xaxis ? c.u : c.v;
+    const double ut = xaxis ? c.v : c.u;
+    s.h = c.h;
+    s.hun = c.wet ? (xaxis ? c.hu : c.hv) : 0.0;
+    s.pi = c.pi;
+    s.z = c.zb;
+    double dq;
+    grass_terms_fast(P, un, ut, c.s2, s.omega, dq);
+    if (!c.wet) {
+        s.omega = 0.0;
+        dq = 0.0;
+    }
+    s.un = un;
+    s.ut = ut;
+    s.tau = c.tau;
+    s.wet = c.wet;
+    s.a_side = c.wet ? c.h * c.sq : 0.0;
+    s.b2_side = c.wet ? fma(s.hun, s.hun, P.g * c.h * c.h * dq) : 0.0;
+    s.moving = c.wet && P.a_g != 0.0 && c.s2 > 0.0;
+    return s;
+}
+
+// ---- interface flux ------------------------------------------------------
+struct Flux {
+    double h, huL, huR, hv, z;  // FaceFlux (src/stepper.cpp:61-67)
+};
+
+// Sample region data: conserved normal discharge, velocity (u(0.0)), relaxed
+// pressure and rate of the state at xi = 0 built by make_state (src/riemann.cpp:60-68).
+template <bool S>
+__device__ __forceinline__ void region_from_tau(double tau, double u, double pi, double omega,
+                                                double& hu, double& u0, double& p, double& w) {
+    if constexpr (S) {
+        const double h = 1.0 / tau;
+        hu = u / tau;
+        u0 = h > 0 ? hu / h : 0.0;
+    } else {
+        hu = u * rcp(tau);
+        u0 = u;
+    }
+    p = pi;
+    w = omega;
+}
+
+// Publish the fluxes of a solved fan: sample at xi = 0 and split the momentum
+// exchange by wave sign (src/riemann.cpp:302-324).
+__device__ __forceinline__ void publish(const double sp[5], const double ex[5], double hu,
+                                        double u0, double p, double w, bool suppressed,
+                                        Flux& F) {
+    F.h = hu;
+    F.z = suppressed ? 0.0 : w;
+    const double base = hu * u0 + p;
+    double mneg = 0, mpos = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        if (sp[k] < 0.0)
+            mneg += ex[k];
+        else
+            mpos += ex[k];
+    }
+    F.huL = base + mneg;
+    F.huR = base - mpos;
+}
+
+__device__ __forceinline__ int first_nonneg(const double sp[5]) {
+    int rg = 5;
+#pragma unroll
+    for (int k = 4; k >= 0; --k)
+        if (sp[k] >= 0.0) rg = k;
+    return rg;
+}
+
+// solve_suppressed: src/riemann.cpp:72-94
+template <bool S>
+__device__ __forceinline__ bool solve_suppressed(const Side& l, const Side& r, double a, double g,
+                                                 Flux& F) {
+    const double tl = l.tau, tr = r.tau;
+    const double ul = l.un, ur = r.un;
+    double ustar, pstar, tsl, tsr;
+    if constexpr (S) {
+        ustar = 0.5 * (ul + ur) + (l.pi - r.pi) / (2.0 * a);
+        pstar = 0.5 * (l.pi + r.pi) + 0.5 * a * (ul - ur);
+        tsl = tl + (ustar - ul) / a;
+        tsr = tr + (ur - ustar) / a;
+    } else {
+        const double ia = rcp(a);
+        ustar = 0.5 * (ul + ur) + (l.pi - r.pi) * (0.5 * ia);
+        pstar = 0.5 * (l.pi + r.pi) + 0.5 * a * (ul - ur);
+        tsl = tl + (ustar - ul) * ia;
+        tsr = tr + (ur - ustar) * ia;
+    }
+    if (!(tsl > 0) || !(tsr > 0)) return false;
+    double sp[5] = {ul - a * tl, ustar, ustar, ustar, ur + a * tr};
+    double ex[5] = {0, 0, g * 0.5 * (l.h + r.h) * (r.z - l.z), 0, 0};
+    const int rg = first_nonneg(sp);
+    double hu, u0, p, w;
+    if (rg == 0) {
+        hu = l.hun; u0 = l.un; p = l.pi; w = l.omega;
+    } else if (rg <= 2) {
+        region_from_tau<S>(tsl, ustar, pstar, l.omega, hu, u0, p, w);
+    } else if (rg <= 4) {
+        region_from_tau<S>(tsr, ustar, pstar, r.omega, hu, u0, p, w);
+    } else {
+        hu = r.hun; u0 = r.un; p = r.pi; w = r.omega;
+    }
+    publish(sp, ex, hu, u0, p, w, true, F);
+    return true;
+}
+
+// solve_solid_outer: src/riemann.cpp:97-146
+template <bool S>
+__device__ __forceinline__ bool solve_solid_outer(const Side& l, const Side& r, double a, double b,
+                                                  double g, Flux& F) {
+    const double tl = l.tau, tr = r.tau;
+    const double ul = l.un, ur = r.un;
+    const double m2 = ul - b * tl;
+    const double m4 = ur + b * tr;
+    const double d = m4 - m2;
+    if (!(d > 0)) return false;
+    const double jz = r.z - l.z;
+    const double jw = r.omega - l.omega;
+    double k, kl, kr, dzl, dzr;
+    if constexpr (S) {
+        k = g / (a * a - b * b);
+        kl = l.pi + a * a * tl;
+        kr = r.pi + a * a * tr;
+        dzl = (m4 * jz - jw) / d;
+        dzr = (m2 * jz - jw) / d;
+    } else {
+        k = g * rcp(a * a - b * b);
+        kl = fma(a * a, tl, l.pi);
+        kr = fma(a * a, tr, r.pi);
+        const double id = rcp(d);
+        dzl = (m4 * jz - jw) * id;
+        dzr = (m2 * jz - jw) * id;
+    }
+    const double zstar = l.z + dzl;
+    const double wstar = l.omega + m2 * dzl;
+    (void)zstar;
+    const double rad1 = tl * tl + 2.0 * k * dzl;
+    const double rad4 = tr * tr + 2.0 * k * dzr;
+    if (!(rad1 > 0) || !(rad4 > 0)) return false;
+    const double t1 = sqrt(rad1);
+    const double t4 = sqrt(rad4);
+    const double u1 = m2 + b * t1;
+    const double u4 = m4 - b * t4;
+    const double p1 = kl - a * a * t1;
+    const double p4 = kr - a * a * t4;
+    double ustar, pstar, t2, t3;
+    if constexpr (S) {
+        ustar = 0.5 * (u1 + u4) + (p1 - p4) / (2.0 * a);
+        pstar = 0.5 * (p1 + p4) + 0.5 * a * (u1 - u4);
+        t2 = t1 + (ustar - u1) / a;
+        t3 = t4 + (u4 - ustar) / a;
+    } else {
+        const double ia = rcp(a);
+        ustar = 0.5 * (u1 + u4) + (p1 - p4) * (0.5 * ia);
+        pstar = 0.5 * (p1 + p4) + 0.5 * a * (u1 - u4);
+        t2 = t1 + (ustar - u1) * ia;
+        t3 = t4 + (u4 - ustar) * ia;
+    }
+    if (!(t2 > 0) || !(t3 > 0)) return false;
+    double sp[5] = {m2, u1 - a * t1, ustar, u4 + a * t4, m4};
+    double ex[5] = {(a * a - b * b) * (t1 - tl), 0, 0, 0, (a * a - b * b) * (tr - t4)};
+    const int rg = first_nonneg(sp);
+    double hu, u0, p, w;
+    switch (rg) {
+        case 0: hu = l.hun; u0 = l.un; p = l.pi; w = l.omega; break;
+        case 1: region_from_tau<S>(t1, u1, p1, wstar, hu, u0, p, w); break;
+        case 2: region_from_tau<S>(t2, ustar, pstar, wstar, hu, u0, p, w); break;
+        case 3: region_from_tau<S>(t3, ustar, pstar, wstar, hu, u0, p, w); break;
+        case 4: region_from_tau<S>(t4, u4, p4, wstar, hu, u0, p, w); break;
+        default: hu = r.hun; u0 = r.un; p = r.pi; w = r.omega; break;
+    }
+    publish(sp, ex, hu, u0, p, w, false, F);
+    return true;
+}
+
+// Newton residual record of solve_fluid_outer (src/riemann.cpp:166-185)
+struct Eval {
+    double t1, t2, t3, t4, dzl, dzr, d, id, r1, r2;
+    bool valid;
+};
+
+struct FluidCtx {
+    double lam, rho, amb, iamb, b, ib, i2b, kappa, jz, jw, k;
+};
+
+template <bool S>
+__device__ __forceinline__ Eval fo_eval(const FluidCtx& c, double m2, double m4) {
+    Eval e;
+    if constexpr (S) {
+        e.t1 = (m2 - c.lam) / c.amb;
+        e.t4 = (c.rho - m4) / c.amb;
+        e.t2 = (m4 - m2 - c.b * c.kappa) / (2.0 * c.b);
+        e.t3 = (m4 - m2 + c.b * c.kappa) / (2.0 * c.b);
+    } else {
+        e.t1 = (m2 - c.lam) * c.iamb;
+        e.t4 = (c.rho - m4) * c.iamb;
+        const double bk = c.b * c.kappa;
+        e.t2 = (m4 - m2 - bk) * c.i2b;
+        e.t3 = (m4 - m2 + bk) * c.i2b;
+    }
+    e.d = m4 - m2;
+    e.valid = e.t1 > 0 && e.t2 > 0 && e.t3 > 0 && e.t4 > 0 && e.d > 0;
+    e.dzl = e.dzr = e.r1 = e.r2 = e.id = 0.0;
+    if (!e.valid) return e;
+    if constexpr (S) {
+        e.dzl = (m4 * c.jz - c.jw) / e.d;
+        e.dzr = (m2 * c.jz - c.jw) / e.d;
+        e.r1 = (e.t1 * e.t1 - e.t2 * e.t2) + (e.t3 * e.t3 - e.t4 * e.t4) + 2.0 * c.k * c.jz;
+        e.r2 = (e.t1 * e.t1 - e.t2 * e.t2) + 2.0 * c.k * e.dzl;
+    } else {
+        e.id = rcp(e.d);
+        e.dzl = (m4 * c.jz - c.jw) * e.id;
+        e.dzr = (m2 * c.jz - c.jw) * e.id;
+        const double q12 = (e.t1 - e.t2) * (e.t1 + e.t2);
+        const double q34 = (e.t3 - e.t4) * (e.t3 + e.t4);
+        e.r1 = q12 + q34 + 2.0 * c.k * c.jz;
+        e.r2 = q12 + 2.0 * c.k * e.dzl;
+    }
+    return e;
+}
+
+__device__ __forceinline__ double res_norm(const Eval& v) {
+    return smax(fabs(v.r1), fabs(v.r2));
+}
+
+// solve_fluid_outer: src/riemann.cpp:152-262 (stopping rule of the code, :201-204)
+template <bool S>
+__device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, double a, double b,
+                                                  double g, Flux& F) {
+    const double tl = l.tau, tr = r.tau;
+    const double ul = l.un, ur = r.un;
+    FluidCtx c;
+    double kl, kr, u0, tsl, tsr;
+    c.b = b;
+    c.amb = a - b;
+    c.jz = r.z - l.z;
+    c.jw = r.omega - l.omega;
+    if constexpr (S) {
+        c.k = g / (a * a - b * b);
+        kl = l.pi + a * a * tl;
+        kr = r.pi + a * a * tr;
+        c.kappa = (kr - kl) / (a * a);
+        c.lam = ul - a * tl;
+        c.rho = ur + a * tr;
+        c.iamb = c.ib = c.i2b = 0.0;
+        u0 = 0.5 * (ul + ur) + (l.pi - r.pi) / (2.0 * a);
+        tsl = tl + (u0 - ul) / a;
+        tsr = tr + (ur - u0) / a;
+    } else {
+        const double a2 = a * a;
+        const double ia = rcp(a);
+        c.k = g * rcp(fma(a, a, -b * b));
+        kl = fma(a2, tl, l.pi);
+        kr = fma(a2, tr, r.pi);
+        c.kappa = (kr - kl) * (ia * ia);
+        c.lam = fma(-a, tl, ul);
+        c.rho = fma(a, tr, ur);
+        c.iamb = rcp(c.amb);
+        c.ib = rcp(b);
+        c.i2b = 0.5 * c.ib;
+        u0 = 0.5 * (ul + ur) + (l.pi - r.pi) * (0.5 * ia);
+        tsl = fma(u0 - ul, ia, tl);
+        tsr = fma(ur - u0, ia, tr);
+    }
+    const double tfloor = 1e-6 * smin(tl, tr);
+    tsl = smax(tsl, tfloor);
+    tsr = smax(tsr, tfloor);
+    double m2 = u0 - b * tsl;
+    double m4 = u0 + b * tsr;
+
+    Eval e = fo_eval<S>(c, m2, m4);
+    if (!e.valid) return false;
+
+    double tmax = tl;
+    tmax = (tmax < tr) ? tr : tmax;
+    tmax = (tmax < e.t1) ? e.t1 : tmax;
+    tmax = (tmax < e.t2) ? e.t2 : tmax;
+    tmax = (tmax < e.t3) ? e.t3 : tmax;
+    tmax = (tmax < e.t4) ? e.t4 : tmax;
+    const double res_scale = tmax * tmax + fabs(2.0 * c.k * c.jz) + fabs(2.0 * c.k * e.dzl) +
+                             fabs(2.0 * c.k * e.dzr);
+    const double tol = 1e-13 * res_scale + 1e-300;
+
+    int it = 0;
+    while (res_norm(e) > tol) {
+        if (++it > kMaxNewton) return false;
+        double j11, j12, j21, j22, det, step2, step4;
+        if constexpr (S) {
+            j11 = 2.0 * e.t1 / c.amb - c.kappa / b;
+            j12 = 2.0 * e.t4 / c.amb + c.kappa / b;
+            j21 = 2.0 * e.t1 / c.amb + e.t2 / b + 2.0 * c.k * e.dzl / e.d;
+            j22 = -e.t2 / b + 2.0 * c.k * (c.jz - e.dzl) / e.d;
+            det = j11 * j22 - j12 * j21;
+            if (det == 0.0 || !isfinite(det)) return false;
+            step2 = (e.r1 * j22 - e.r2 * j12) / det;
+            step4 = (e.r2 * j11 - e.r1 * j21) / det;
+        } else {
+            const double kib = c.kappa * c.ib;
+            const double t1a = 2.0 * e.t1 * c.iamb;
+            const double tk = 2.0 * c.k * e.id;
+            j11 = t1a - kib;
+            j12 = fma(2.0 * e.t4, c.iamb, kib);
+            j21 = fma(e.t2, c.ib, fma(tk, e.dzl, t1a));
+            j22 = fma(-e.t2, c.ib, tk * (c.jz - e.dzl));
+            det = j11 * j22 - j12 * j21;
+            if (det == 0.0 || !isfinite(det)) return false;
+            const double idet = rcp(det);
+            step2 = (e.r1 * j22 - e.r2 * j12) * idet;
+            step4 = (e.r2 * j11 - e.r1 * j21) * idet;
+        }
+        double damp = 1.0;
+        bool accepted = false;
+        const double rn = res_norm(e);
+        for (int bt = 0; bt < 40; ++bt) {
+            const Eval trial = fo_eval<S>(c, m2 - damp * step2, m4 - damp * step4);
+            if (trial.valid && (res_norm(trial) < rn || res_norm(trial) <= tol)) {
+                m2 -= damp * step2;
+                m4 -= damp * step4;
+                e = trial;
+                accepted = true;
+                break;
+            }
+            damp *= 0.5;
+        }
+        if (!accepted) return false;
+    }
+
+    const double ustar = 0.5 * (m2 + m4 - b * c.kappa);
+    const double wstar = l.omega + m2 * e.dzl;
+    const double a2 = a * a;
+    double sp[5] = {c.lam, m2, ustar, m4, c.rho};
+    double ex[5] = {0, (a2 - b * b) * (e.t2 - e.t1), 0, (a2 - b * b) * (e.t4 - e.t3), 0};
+    const int rg = first_nonneg(sp);
+    double hu, uu, p, w;
+    switch (rg) {
+        case 0: hu = l.hun; uu = l.un; p = l.pi; w = l.omega; break;
+        case 1: region_from_tau<S>(e.t1, c.lam + a * e.t1, kl - a2 * e.t1, l.omega, hu, uu, p, w); break;
+        case 2: region_from_tau<S>(e.t2, ustar, kl - a2 * e.t2, wstar, hu, uu, p, w); break;
+        case 3: region_from_tau<S>(e.t3, ustar, kr - a2 * e.t3, wstar, hu, uu, p, w); break;
+        case 4: region_from_tau<S>(e.t4, c.rho - a * e.t4, kr - a2 * e.t4, r.omega, hu, uu, p, w); break;
+        default: hu = r.hun; uu = r.un; p = r.pi; w = r.omega; break;
+    }
+    publish(sp, ex, hu, uu, p, w, false, F);
+    return true;
+}
+
+// interface_riemann (src/riemann.cpp:266-338) + the celerity pair of
+// bounds_impl (src/relax_state.cpp:25-53) + the transverse flux of solve_face
+// (src/stepper.cpp:87).  Returns false when no positive fan exists after
+// kMaxEnlarge enlargements (the reference throws runtime_error).
+template <bool S>
+__device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const Side& r, Flux& F) {
+    F.h = F.huL = F.huR = F.hv = F.z = 0.0;
+    if (!l.wet && !r.wet) return true;  // inert interface: a = b = 0
+    const double a0 = P.safety * smax(smax(0.0, l.a_side), r.a_side);
+    const double b0 =
+        (l.moving || r.moving) ? P.safety * sqrt(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
+    double a = a0, b = b0;
+    bool ok = false;
+    for (int attempt = 0; attempt <= kMaxEnlarge; ++attempt) {
+        double ae = a, be = b;
+        if (be >= kSuppressB) {
+            if (ae >= be)
+                ae = smax(ae, kGap * be);
+            else
+                be = smax(be, kGap * ae);
+        }
+        if (be < kSuppressB)
+            ok = solve_suppressed<S>(l, r, ae, P.g, F);
+        else if (be > ae)
+            ok = solve_solid_outer<S>(l, r, ae, be, P.g, F);
+        else
+            ok = solve_fluid_outer<S>(l, r, ae, be, P.g, F);
+        if (ok) break;
+        a *= 2.0;
+        if (b > 0) b *= 2.0;
+    }
+    if (!ok) {
+        F.h = F.huL = F.huR = F.hv = F.z = 0.0;
+        return false;
+    }
+    F.hv = F.h * (F.h > 0 ? l.ut : F.h < 0 ? r.ut : 0.0);
+    return true;
+}
+
+// axis_speed: src/stepper.cpp:30-36 (STRICT, on primitives)
+__device__ __forceinline__ double axis_speed_ref(const Params& P, double h, double un, double ut) {
+    const double fluid = fabs(un) + sqrt(P.g * h);
+    const double dq = normal_flux_derivative_ref(P, h, un, ut);
+    const double solid = fabs(un) + sqrt(un * un + P.g * dq);
+    return smax(fluid, solid);
+}
+
+// check_depth: src/stepper.cpp:91-100.  Returns false on a real violation.
+__device__ __forceinline__ bool check_depth(double& h, double href) {
+    if (h >= 0) return true;
+    if (h > -1e-12 * smax(href, 1.0)) {
+        h = 0;
+        return true;
+    }
+    return false;
+}
+
+}  // namespace silt_dev

@@ -1,0 +1,18 @@
+// silt_physics_params.h — per-launch physical parameters (host + device).
+#pragma once
+
+namespace silt_dev {
+
+// error bits raised on device (mapped to the reference's exceptions on host)
+constexpr unsigned kErrNegDepth = 1u;  // check_depth (src/stepper.cpp:91-100)
+constexpr unsigned kErrRiemann = 2u;   // interface_riemann (src/riemann.cpp:332-337)
+constexpr unsigned kErrDry = 4u;       // cfl_dt all dry (src/stepper.cpp:56)
+
+// Physics (include/silt/physics.hpp:7-11) + Grass law (bedload.hpp:32-52) +
+// the interface safety factor (Scenario::safety, scenarios.hpp:47).
+struct Params {
+    double g, h_dry, a_g, m_g, safety, half_g;
+    int m3;  // m_g == 3: closed-form Grass terms in the FAST variant
+};
+
+}  // namespace silt_dev
