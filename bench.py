@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native relaxation time step (arXiv 1307.0491).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4|C3|C5]
+                    [--impl ours|reference] [--variant fast|strict]
+
+Metric (BASELINE.json): fp64 2D cell-updates/s, whole job, with the fraction
+of the HBM roofline.  A "step" is one time step of the fused kernel over the
+whole grid (all strips).  Default workload C4 = the 16384^2 dune of
+BASELINE.json configs[3] (the north star's strong-scaling grid; 8.6 GB of
+state per copy, far larger than L2, so no L2 flush is needed).  N > 1 runs
+under torchrun: one process per GPU, row strips, NCCL halo rows + MAX
+all-reduce of the CFL speeds (paper_1307_0491_b200.distributed).
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, the unmodified reference core) on this host's cores over a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_CELL = 64  # h, hu, hv, zb fp64 read once + written once
+FALLBACK_HBM_GBS = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+WORKLOADS = {
+    # name: (builder kwargs, description)
+    "C3": dict(kind="dune", n=1024, a_g=0.001, cfl=0.5),
+    "C4": dict(kind="dune", n=16384, a_g=0.001, cfl=0.5),
+    "C5": dict(kind="random", nx=8192, ny_per_gpu=4096, a_g=0.01, cfl=0.4),
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_global_problem(wl: str, world: int):
+    from paper_1307_0491_b200 import abi
+    w = WORKLOADS[wl]
+    if w["kind"] == "dune":
+        n = w["n"]
+        p = abi.make_problem(2, n, n, 1000.0 / n, 1000.0 / n, a_g=w["a_g"], cfl=w["cfl"])
+    else:
+        ny = w["ny_per_gpu"] * world
+        p = abi.make_problem(2, w["nx"], ny, 1.0, 1.0, a_g=w["a_g"], cfl=w["cfl"])
+    return p
+
+
+def device_initial_rows(wl: str, p, j0: int, nrows: int, device):
+    """Initial AoS rows [j0, j0+nrows) built on the device (bitwise equal to
+    scenarios.dune_2d / the reference's sine_bump construction)."""
+    import numpy as np
+    import torch
+    from paper_1307_0491_b200 import scenarios as S
+    w = WORKLOADS[wl]
+    nx = p.nx
+    out = torch.zeros((nrows, nx, 4), dtype=torch.float64, device=device)
+    if w["kind"] == "dune":
+        wx = torch.from_numpy(S._sine_bump(S._centres(nx, p.dx), 300.0, 200.0)).to(device)
+        wy_all = S._sine_bump(S._centres(p.ny, p.dy), 400.0, 200.0)
+        wy = torch.from_numpy(np.ascontiguousarray(wy_all[j0:j0 + nrows])).to(device)
+        zb = 0.1 + torch.outer(wy, wx)
+        out[..., 0] = 10.0 - zb
+        out[..., 1] = 10.0
+        out[..., 3] = zb
+    else:
+        # random bed generated per strip on the host (counter-based, seeded)
+        _, init, _ = S.random_bed_2d(nx, p.ny, a_g=p.a_g, cfl=p.cfl) if p.ny * nx <= (1 << 26) \
+            else (None, None, None)
+        if init is None:
+            g = torch.Generator(device=device)
+            g.manual_seed(1307 + j0)
+            noise = torch.randn((nrows, nx), generator=g, device=device, dtype=torch.float64)
+            kx = torch.fft.rfftfreq(nx, device=device, dtype=torch.float64)
+            ky = torch.fft.fftfreq(nrows, device=device, dtype=torch.float64)
+            filt = torch.exp(-2.0 * (math.pi * 20.0) ** 2 * (ky[:, None] ** 2 + kx[None, :] ** 2))
+            grf = torch.fft.irfft2(torch.fft.rfft2(noise) * filt, s=(nrows, nx))
+            grf = (grf - grf.mean()) / grf.std()
+            zb = 0.1 + 0.05 * grf.clamp(-1.0, 1.0)
+            out[..., 0] = 2.0 - zb
+            out[..., 1] = 0.5 + torch.rand((nrows, nx), generator=g, device=device, dtype=torch.float64)
+            out[..., 2] = -0.1 + 0.2 * torch.rand((nrows, nx), generator=g, device=device,
+                                                  dtype=torch.float64)
+            out[..., 3] = zb
+        else:
+            out.copy_(torch.from_numpy(init[j0:j0 + nrows]))
+    return out
+
+
+def cpu_reference_sample(wl: str, steps: int, threads: int):
+    """The reference's CPU run_parallel (oracle/_ref) on a bounded row sample
+    of the workload; returns (cell-updates/s, description)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_1307_0491_b200 import abi, scenarios as S
+    w = WORKLOADS[wl]
+    if w["kind"] == "dune":
+        n = w["n"]
+        rows = 96 if n >= 8192 else min(n, 256)
+        # a band of C4/C3 rows through the mound (y in [400, 600] m)
+        j0 = int(0.45 * n)
+        p_full = abi.make_problem(2, n, n, 1000.0 / n, 1000.0 / n, a_g=w["a_g"], cfl=w["cfl"])
+        wx = S._sine_bump(S._centres(n, p_full.dx), 300.0, 200.0)
+        wy = S._sine_bump(S._centres(n, p_full.dy), 400.0, 200.0)[j0:j0 + rows]
+        init = np.zeros((rows, n, 4))
+        zb = 0.1 + np.multiply.outer(wy, wx)
+        init[..., 0] = 10.0 - zb
+        init[..., 1] = 10.0
+        init[..., 3] = zb
+        p = abi.make_problem(2, n, rows, p_full.dx, p_full.dy, a_g=w["a_g"], cfl=w["cfl"])
+        desc = f"{wl} rows [{j0},{j0 + rows}) x {n} cols"
+    else:
+        p, init, _ = S.random_bed_2d(w["nx"], 64, a_g=w["a_g"], cfl=w["cfl"])
+        desc = f"{wl} {w['nx']} x 64 rows"
+    R = O.reference() if O.have_reference() else None
+    kind = "reference"
+    if R is None:
+        R, kind = O.restatement(), "port"
+    t0 = time.perf_counter()
+    if kind == "reference":
+        _, _, n_steps, comp, _ = R.run_parallel(p, init, 1, min(threads, p.ny),
+                                                max_steps=steps, want_field=False)
+        secs = comp
+    else:
+        _, _, n_steps, _ = R.run(p, init, max_steps=steps)
+        secs = time.perf_counter() - t0
+        threads = 1
+    cells = p.nx * p.ny * n_steps
+    return cells / secs, f"{desc}, {n_steps} steps", kind, threads
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    total_cells = 0.0
+    total_secs = 0.0
+    for s in range(args.warmup + args.steps):
+        rate, desc, kind, used = cpu_reference_sample(args.workload, 1, threads)
+        if s >= args.warmup:
+            total_secs += 1.0 / rate
+            total_cells += 1.0
+    value = total_cells / total_secs
+    line = {
+        "metric": "cell-updates/s (fp64, 2D)", "value": value, "unit": "cell-updates/s",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": used, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="fast", choices=["fast", "strict"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    from paper_1307_0491_b200 import abi, native
+    from paper_1307_0491_b200.distributed import StripRunner, init_dist
+
+    world, rank, local = init_dist(args.gpus)
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    variant = abi.VARIANT_FAST if args.variant == "fast" else abi.VARIANT_STRICT
+    p = build_global_problem(args.workload, world)
+    runner = StripRunner(p, world, rank, device=local, variant=variant)
+    j0, nrows = runner.j0, runner.nrows
+    init = device_initial_rows(args.workload, p, j0, nrows, device)
+    runner.upload_device(init)
+    del init
+    total = args.warmup + args.steps
+    runner.begin(max_steps=total + 1)
+    runner.step(args.warmup)
+    runner.synchronize()
+
+    stream = runner.torch_stream
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    n0 = runner.launch_count()
+    runner.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        runner.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    runner.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = runner.launch_count() - n0
+    ms = runner.max_over_ranks(ms)
+    st = runner.status()
+    assert st.steps == total, (st.steps, total)
+
+    cells = p.nx * p.ny
+    value = cells * args.steps / (ms / 1e3)
+    ms_step = ms / args.steps
+    peak, peak_src = peaks()
+    per_gpu_cells = nrows * p.nx
+    achieved = per_gpu_cells * BYTES_PER_CELL / (ms_step / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tj = json.load(fh)
+        tr = tj.get(args.workload)
+        if tr:
+            traffic = tr["dram_bytes_per_launch"] * (per_gpu_cells / tr["cells"])
+    except Exception:
+        pass
+
+    # end to end through the public API (silt_run semantics): pinned host
+    # field -> device, K steps, device -> pinned host
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((nrows, p.nx, 4), dtype=torch.float64, pin_memory=True)
+        host.copy_(device_initial_rows(args.workload, p, j0, nrows, device).cpu())
+        out = torch.empty_like(host, pin_memory=True)
+        runner2 = StripRunner(p, world, rank, device=local, variant=variant)
+        runner2.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        runner2.upload_host(host)
+        runner2.begin(max_steps=args.steps)
+        runner2.step(args.steps)
+        runner2.download_host(out)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        runner2.barrier()
+        el = runner.max_over_ranks(el)
+        e2e = {"value": cells * args.steps / el, "unit": "cell-updates/s",
+               "h2d_bytes_per_step": int(host.numel() * 8 * world / args.steps),
+               "d2h_bytes_per_step": int(out.numel() * 8 * world / args.steps),
+               "timing": "wall clock around upload+begin+K steps+download, max over ranks"}
+        runner2.close()
+        del host, out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rate, desc, kind, used = cpu_reference_sample(args.workload, 3, os.cpu_count() or 1)
+            cpu = {"value": rate, "unit": "cell-updates/s", "cores": used, "kind": kind,
+                   "sample": desc}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "cell-updates/s (fp64, 2D)",
+            "value": value,
+            "unit": "cell-updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak" if WORKLOADS[args.workload]["kind"] == "random" else "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "variant": args.variant,
+            "config": {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
+                       "nx": p.nx, "ny": p.ny, "rows_per_gpu": nrows,
+                       "parallelism": f"row strips x{world}",
+                       "l2": "state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "note": "algorithmic 64 B/cell-update / step-kernel duration"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    runner.close()
+    runner.shutdown()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -75,8 +75,8 @@ enum { SILT_WEST = 0, SILT_EAST = 1, SILT_SOUTH = 2, SILT_NORTH = 3 };
 
 /* Numerical variant of the kernels. FAST: contracted FMAs, reciprocals,
  * closed-form Grass terms; parity to 1e-9 normwise.  STRICT: the reference's
- * operation order, no FMA contraction, IEEE division and a correctly rounded
- * hypot (bitwise-comparable with the CPU reference). */
+ * operation order, no FMA contraction, IEEE division and glibc's hypot
+ * algorithm (bitwise-identical to the CPU reference). */
 enum { SILT_VARIANT_FAST = 0, SILT_VARIANT_STRICT = 1 };
 
 /* Run state reported by silt_solver_status. */
@@ -149,6 +149,10 @@ typedef struct silt_exchange {
 typedef struct silt_solver silt_solver;
 
 int silt_abi_version(void);
+/* sizeof of silt_bc, silt_problem, silt_strip, silt_run_plan, silt_status,
+ * silt_exchange (in that order) into sizes[0..n); lets bindings verify their
+ * mirrors without a GPU. */
+int silt_abi_sizes(int64_t* sizes, int n);
 const char* silt_last_error(void);
 int silt_device_count(int* count);
 

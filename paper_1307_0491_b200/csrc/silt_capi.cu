@@ -182,6 +182,13 @@ extern "C" {
 
 int silt_abi_version(void) { return SILT_ABI_VERSION; }
 
+int silt_abi_sizes(int64_t* sizes, int n) {
+    const int64_t all[6] = {sizeof(silt_bc),       sizeof(silt_problem), sizeof(silt_strip),
+                            sizeof(silt_run_plan), sizeof(silt_status),  sizeof(silt_exchange)};
+    for (int k = 0; k < n && k < 6; ++k) sizes[k] = all[k];
+    return SILT_OK;
+}
+
 const char* silt_last_error(void) { return g_err.c_str(); }
 
 int silt_device_count(int* count) {

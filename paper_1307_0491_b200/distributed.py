@@ -1,0 +1,254 @@
+"""Row-strip domain decomposition across GPUs (one process per GPU).
+
+The reference runs the paper's MPI decomposition as SPMD threads
+(run_parallel, src/parallel.cpp:261-386): Cartesian blocks (partition,
+:150-177), a one-cell pull halo (pull_halo, :43-84) and an exact-min global dt
+(global_dt, :200-206).  Here every rank owns a strip of whole rows
+(Topology{px=1, py=G}, remainder rows to the lowest ranks as in block_range,
+:25-30) resident in its GPU's HBM.  Per step, in stream order and with no host
+synchronisation:
+
+  1. the fused step kernel advances the strip and writes its edge rows into
+     send buffers plus its CFL speed maxima into the reduction slot;
+  2. ghost rows move to the neighbours (NCCL send/recv: ``batch_isend_irecv``);
+  3. the two axis-speed maxima are all-reduced with MAX (16 bytes).  Because
+     correctly rounded division is monotone, min over ranks of
+     cfl*min(dx/sx_r, dy/sy_r) == cfl*min(dx/max sx, dy/max sy): the dt every
+     rank derives on device equals global_dt bit for bit.
+
+``depth hmax`` stays per strip (the reference's per-worker check_depth).
+The same driver runs on CPU with the gloo backend for the tests, with any
+object that implements the strip-solver interface below.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import abi
+
+
+def block_range(n: int, parts: int, r: int):
+    """block_range (src/parallel.cpp:25-30): (offset, count)."""
+    base, rem = divmod(n, parts)
+    count = base + (1 if r < rem else 0)
+    offset = r * base + min(r, rem)
+    return offset, count
+
+
+def neighbours(rank: int, world: int, periodic_y: bool):
+    """Topology::neighbor (src/parallel.cpp:136-148) for px = 1, py = world:
+    (south rank or None, north rank or None)."""
+    south = rank - 1 if rank > 0 else (world - 1 if periodic_y and world > 1 else None)
+    north = rank + 1 if rank < world - 1 else (0 if periodic_y and world > 1 else None)
+    return south, north
+
+
+def init_dist(gpus: int = 1, backend: str | None = None):
+    """(world, rank, local_rank); initialises torch.distributed when world > 1."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            if backend is None:
+                backend = "nccl" if torch.cuda.is_available() else "gloo"
+            kw = {}
+            if backend == "nccl":
+                kw["device_id"] = torch.device("cuda", local)
+            dist.init_process_group(backend, **kw)
+    return world, rank, local
+
+
+class _CAI:
+    """Zero-copy view of a device buffer for torch (CUDA array interface)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class StripRunner:
+    """One rank's strip: a solver + the per-step halo/dt exchange.
+
+    ``solver`` defaults to the CUDA solver (native.Solver) on ``device``; tests
+    pass a CPU stand-in with the same interface.
+    """
+
+    def __init__(self, problem, world: int, rank: int, device: int = 0,
+                 variant: int = abi.VARIANT_FAST, solver_factory=None):
+        self.problem = problem
+        self.world, self.rank = world, rank
+        ny = 1 if problem.dim == 1 else problem.ny
+        if world > ny:
+            raise ValueError("partition: every worker needs at least one cell per axis")
+        if problem.dim == 1 and world > 1:
+            raise ValueError("partition: 1D grids require py == 1")
+        self.j0, self.nrows = block_range(ny, world, rank)
+        periodic_y = problem.dim == 2 and problem.bc[abi.SOUTH].type == abi.BC_PERIODIC
+        self.south, self.north = neighbours(rank, world, periodic_y)
+        strip = abi.SiltStrip(self.j0, self.nrows, int(self.south is not None),
+                              int(self.north is not None))
+        self.torch_stream = None
+        if solver_factory is None:
+            import torch
+            from . import native
+            self.solver = native.Solver(problem, strip, device, variant)
+            self.torch_stream = torch.cuda.Stream(device=device)
+            self.solver.set_stream(self.torch_stream.cuda_stream)
+            self.device = torch.device("cuda", device)
+            ex = self.solver.exchange_ptrs()
+            n = ex.row_doubles
+            self._send_s = self._wrap(ex.send_south, n)
+            self._send_n = self._wrap(ex.send_north, n)
+            self._recv_s = self._wrap(ex.recv_south, n)
+            self._recv_n = self._wrap(ex.recv_north, n)
+        else:
+            self.solver = solver_factory(problem, strip)
+            self.device = None
+            self._send_s, self._send_n, self._recv_s, self._recv_n = self.solver.exchange_tensors()
+        self._dist = None
+        if world > 1:
+            import torch.distributed as dist
+            self._dist = dist
+
+    def _wrap(self, ptr, n):
+        if not ptr:
+            return None
+        import torch
+        return torch.as_tensor(_CAI(ptr, n), device=self.device)
+
+    def _slot(self):
+        if self.torch_stream is None:
+            return self.solver.reduce_slot_tensor()
+        import torch
+        return torch.as_tensor(_CAI(self.solver.reduce_slot(), 2), device=self.device)
+
+    # ---- exchange ---------------------------------------------------------
+    def _exchange(self):
+        """Ghost rows of the newest state to the neighbours, then MAX of the
+        axis speeds.  Order per rank: send north, recv south, send south, recv
+        north — consistent pairing also when south == north (periodic, G=2)."""
+        if self.world == 1:
+            return
+        dist = self._dist
+        ops = []
+        if self.north is not None:
+            ops.append(dist.P2POp(dist.isend, self._send_n, self.north))
+        if self.south is not None:
+            ops.append(dist.P2POp(dist.irecv, self._recv_s, self.south))
+        if self.south is not None:
+            ops.append(dist.P2POp(dist.isend, self._send_s, self.south))
+        if self.north is not None:
+            ops.append(dist.P2POp(dist.irecv, self._recv_n, self.north))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        dist.all_reduce(self._slot(), op=dist.ReduceOp.MAX)
+
+    def _ctx(self):
+        if self.torch_stream is None:
+            import contextlib
+            return contextlib.nullcontext()
+        import torch
+        return torch.cuda.stream(self.torch_stream)
+
+    # ---- solver interface ----------------------------------------------------
+    def upload_device(self, tensor):
+        self.solver.upload_device(tensor.data_ptr())
+        if self.torch_stream is not None:
+            self.torch_stream.synchronize()
+
+    def upload_host(self, array):
+        if hasattr(array, "data_ptr"):
+            import ctypes as C
+            self.solver.L.silt_solver_upload(self.solver.h,
+                                             C.cast(array.data_ptr(), C.POINTER(C.c_double)))
+        else:
+            self.solver.upload(array)
+
+    def download_host(self, out):
+        if hasattr(out, "data_ptr"):
+            import ctypes as C
+            from .native import check
+            check(self.solver.L.silt_solver_download(self.solver.h,
+                                                     C.cast(out.data_ptr(), C.POINTER(C.c_double))))
+            return out
+        return self.solver.download(out)
+
+    def begin(self, t_end: float = np.inf, max_steps: int = -1, snapshots=(), dt_cap: int = 0):
+        with self._ctx():
+            self.solver.begin(t_end=t_end, max_steps=max_steps, snapshots=snapshots,
+                              dt_cap=dt_cap)
+            self._exchange()
+
+    def step(self, n: int = 1):
+        with self._ctx():
+            if self.world == 1:
+                self.solver.step(n)
+                return
+            for _ in range(n):
+                self.solver.step(1)
+                self._exchange()
+
+    def status(self):
+        return self.solver.status()
+
+    def resume(self):
+        self.solver.resume()
+
+    def launch_count(self) -> int:
+        return self.solver.launch_count()
+
+    def synchronize(self):
+        if self.torch_stream is not None:
+            self.torch_stream.synchronize()
+
+    def barrier(self):
+        if self._dist is not None:
+            self._dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        if self._dist is None:
+            return v
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64,
+                         device=self.device if self.device is not None else "cpu")
+        self._dist.all_reduce(t, op=self._dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def run(self, batch: int = 16, on_snapshot=None):
+        """run_parallel's loop: advance until DONE, gathering at snapshots."""
+        while True:
+            self.step(batch)
+            st = self.status()
+            if st.state == abi.STATE_PAUSED:
+                if on_snapshot is not None:
+                    f = self.gather()
+                    if self.rank == 0:
+                        on_snapshot(st.t, f)
+                self.resume()
+                continue
+            if st.state == abi.STATE_DONE:
+                return st
+
+    def gather(self):
+        """gather (src/parallel.cpp:179-190): the global field on rank 0."""
+        local = self.solver.download()
+        if self.world == 1:
+            return local
+        parts = [None] * self.world if self.rank == 0 else None
+        self._dist.gather_object(local, parts, dst=0)
+        if self.rank != 0:
+            return None
+        return np.concatenate(parts, axis=0)
+
+    def close(self):
+        self.solver.close()
+
+    def shutdown(self):
+        if self._dist is not None and self._dist.is_initialized():
+            self._dist.destroy_process_group()

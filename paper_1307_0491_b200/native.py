@@ -1,0 +1,266 @@
+"""ctypes binding of libsilt_b200.so (include/silt_cuda.h).
+
+The CUDA library is the only compute path: there is no CPU fallback.  If the
+library is missing, importing the bindings raises ``SiltLibraryMissing``.
+Status codes map onto the reference's exception classes:
+SILT_ERR_INVALID -> InvalidArgument (std::invalid_argument),
+SILT_ERR_RUNTIME -> SiltRuntimeError (std::runtime_error).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+from .abi import SiltExchange, SiltProblem, SiltRunPlan, SiltStatus, SiltStrip
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsilt_b200.so")
+
+
+class SiltLibraryMissing(ImportError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class SiltRuntimeError(RuntimeError):
+    """std::runtime_error in the reference."""
+
+
+class SiltCudaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+_P = C.POINTER(SiltProblem)
+_D = C.POINTER(C.c_double)
+_VP = C.c_void_p
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SiltLibraryMissing(
+            f"{LIB_PATH} not built; run `python -m paper_1307_0491_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    sigs = {
+        "silt_abi_version": ([], C.c_int),
+        "silt_abi_sizes": ([C.POINTER(C.c_int64), C.c_int], C.c_int),
+        "silt_last_error": ([], C.c_char_p),
+        "silt_device_count": ([C.POINTER(C.c_int)], C.c_int),
+        "silt_solver_create": ([_P, C.POINTER(SiltStrip), C.c_int, C.c_int, C.POINTER(_VP)], C.c_int),
+        "silt_solver_destroy": ([_VP], C.c_int),
+        "silt_solver_set_stream": ([_VP, _VP], C.c_int),
+        "silt_solver_upload": ([_VP, _D], C.c_int),
+        "silt_solver_download": ([_VP, _D], C.c_int),
+        "silt_solver_upload_device": ([_VP, _VP], C.c_int),
+        "silt_solver_download_device": ([_VP, _VP], C.c_int),
+        "silt_solver_set_ghosts": ([_VP, _D, _D, _D, _D], C.c_int),
+        "silt_solver_begin": ([_VP, C.POINTER(SiltRunPlan)], C.c_int),
+        "silt_solver_step": ([_VP, C.c_int], C.c_int),
+        "silt_solver_step_fixed": ([_VP, C.c_double], C.c_int),
+        "silt_solver_status": ([_VP, C.POINTER(SiltStatus)], C.c_int),
+        "silt_solver_resume": ([_VP], C.c_int),
+        "silt_solver_dt_log": ([_VP, _D, C.c_int64], C.c_int),
+        "silt_solver_cfl_dt": ([_VP, _D], C.c_int),
+        "silt_solver_reduce_slot": ([_VP, C.POINTER(_VP)], C.c_int),
+        "silt_solver_exchange_ptrs": ([_VP, C.POINTER(SiltExchange)], C.c_int),
+        "silt_solver_launch_count": ([_VP, C.POINTER(C.c_int64)], C.c_int),
+        "silt_run": ([_P, _D, C.POINTER(SiltRunPlan), C.c_int, _D, _D, C.c_int64,
+                      C.POINTER(SiltStatus)], C.c_int),
+        "silt_cfl_dt": ([_P, _D, C.c_int, _D], C.c_int),
+        "silt_step_padded": ([_P, _D, C.c_double, C.c_int], C.c_int),
+        "silt_riemann_batch": ([_P, _D, _D, C.c_int64, C.c_int, C.c_int, _D], C.c_int),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.silt_abi_version() != abi.SILT_ABI_VERSION:
+        raise SiltLibraryMissing("libsilt_b200.so ABI version mismatch; rebuild")
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc == abi.SILT_OK:
+        return
+    msg = lib().silt_last_error().decode()
+    if rc == abi.SILT_ERR_INVALID:
+        raise InvalidArgument(msg)
+    if rc == abi.SILT_ERR_RUNTIME:
+        raise SiltRuntimeError(msg)
+    if rc == abi.SILT_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise SiltCudaError(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+def _plan(t_end: float, max_steps: int, snapshots, dt_cap: int):
+    snaps = np.ascontiguousarray(np.asarray(snapshots, dtype=np.float64).reshape(-1))
+    plan = SiltRunPlan(float(t_end), int(max_steps),
+                       _dp(snaps) if snaps.size else None, int(snaps.size), int(dt_cap))
+    return plan, snaps
+
+
+class Solver:
+    """One strip (or the whole grid) resident on one GPU."""
+
+    def __init__(self, problem: SiltProblem, strip: SiltStrip | None = None, device: int = 0,
+                 variant: int = abi.VARIANT_FAST):
+        self.L = lib()
+        self.problem = problem
+        self.h = _VP()
+        check(self.L.silt_solver_create(C.byref(problem), C.byref(strip) if strip else None,
+                                        device, variant, C.byref(self.h)))
+        ny = 1 if problem.dim == 1 else problem.ny
+        self.nx = problem.nx
+        self.ny = strip.ny_local if strip else ny
+
+    def close(self):
+        if self.h:
+            self.L.silt_solver_destroy(self.h)
+            self.h = _VP()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # data movement ---------------------------------------------------------
+    def upload(self, field: np.ndarray):
+        field = np.ascontiguousarray(field, dtype=np.float64)
+        assert field.size == 4 * self.nx * self.ny
+        check(self.L.silt_solver_upload(self.h, _dp(field)))
+
+    def upload_device(self, ptr: int):
+        check(self.L.silt_solver_upload_device(self.h, ptr))
+
+    def download(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.ny, self.nx, 4))
+        check(self.L.silt_solver_download(self.h, _dp(out)))
+        return out
+
+    def download_device(self, ptr: int):
+        check(self.L.silt_solver_download_device(self.h, ptr))
+
+    def set_stream(self, stream_ptr: int):
+        check(self.L.silt_solver_set_stream(self.h, stream_ptr))
+
+    # run control -------------------------------------------------------------
+    def begin(self, t_end: float = np.inf, max_steps: int = -1, snapshots=(), dt_cap: int = 0):
+        plan, keep = _plan(t_end, max_steps, snapshots, dt_cap)
+        check(self.L.silt_solver_begin(self.h, C.byref(plan)))
+        del keep
+
+    def step(self, n: int = 1):
+        check(self.L.silt_solver_step(self.h, int(n)))
+
+    def step_fixed(self, dt: float):
+        check(self.L.silt_solver_step_fixed(self.h, float(dt)))
+
+    def status(self) -> SiltStatus:
+        st = SiltStatus()
+        check(self.L.silt_solver_status(self.h, C.byref(st)))
+        return st
+
+    def resume(self):
+        check(self.L.silt_solver_resume(self.h))
+
+    def dt_log(self, n: int) -> np.ndarray:
+        out = np.empty(n)
+        check(self.L.silt_solver_dt_log(self.h, _dp(out), int(n)))
+        return out
+
+    def cfl_dt(self) -> float:
+        dt = C.c_double()
+        check(self.L.silt_solver_cfl_dt(self.h, C.byref(dt)))
+        return dt.value
+
+    def reduce_slot(self) -> int:
+        p = _VP()
+        check(self.L.silt_solver_reduce_slot(self.h, C.byref(p)))
+        return p.value
+
+    def exchange_ptrs(self) -> SiltExchange:
+        ex = SiltExchange()
+        check(self.L.silt_solver_exchange_ptrs(self.h, C.byref(ex)))
+        return ex
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        check(self.L.silt_solver_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def run(self, batch: int = 32, on_snapshot=None) -> SiltStatus:
+        """Advance until DONE; PAUSED snapshots call on_snapshot(t, field)."""
+        while True:
+            self.step(batch)
+            st = self.status()
+            if st.state == abi.STATE_PAUSED:
+                if on_snapshot is not None:
+                    on_snapshot(st.t, self.download())
+                self.resume()
+                continue
+            if st.state == abi.STATE_DONE:
+                return st
+
+
+# ---- one-shot conveniences (mirror the reference free functions) -------------
+def run(problem: SiltProblem, init: np.ndarray, *, t_end: float = np.inf, max_steps: int = -1,
+        snapshots=(), variant: int = abi.VARIANT_FAST, dt_log: bool = True):
+    """run_serial on one GPU: returns (final field, t, steps, dt log)."""
+    L = lib()
+    init = np.ascontiguousarray(init, dtype=np.float64)
+    out = np.empty_like(init)
+    cap = (max_steps if max_steps >= 0 else 1 << 20) if dt_log else 0
+    log = np.empty(max(cap, 1))
+    plan, keep = _plan(t_end, max_steps, snapshots, cap)
+    st = SiltStatus()
+    check(L.silt_run(C.byref(problem), _dp(init), C.byref(plan), variant, _dp(out),
+                     _dp(log) if dt_log else None, cap, C.byref(st)))
+    del keep
+    return out, st.t, st.steps, (log[:min(st.steps, cap)].copy() if dt_log else None)
+
+
+def cfl_dt(problem: SiltProblem, field: np.ndarray, variant: int = abi.VARIANT_FAST) -> float:
+    field = np.ascontiguousarray(field, dtype=np.float64)
+    dt = C.c_double()
+    check(lib().silt_cfl_dt(C.byref(problem), _dp(field), variant, C.byref(dt)))
+    return dt.value
+
+
+def step_padded(problem: SiltProblem, padded: np.ndarray, dt: float,
+                variant: int = abi.VARIANT_FAST) -> np.ndarray:
+    padded = np.array(padded, dtype=np.float64, order="C", copy=True)
+    check(lib().silt_step_padded(C.byref(problem), _dp(padded), float(dt), variant))
+    return padded
+
+
+def faces(problem: SiltProblem, left: np.ndarray, right: np.ndarray, axis: int,
+          variant: int = abi.VARIANT_FAST) -> np.ndarray:
+    left = np.ascontiguousarray(left, dtype=np.float64).reshape(-1, 4)
+    right = np.ascontiguousarray(right, dtype=np.float64).reshape(-1, 4)
+    out = np.empty((left.shape[0], 5))
+    check(lib().silt_riemann_batch(C.byref(problem), _dp(left), _dp(right), left.shape[0],
+                                   axis, variant, _dp(out)))
+    return out
