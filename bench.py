@@ -47,6 +47,7 @@ WORKLOADS = {
     # name: (builder kwargs, description)
     "C3": dict(kind="dune", n=1024, a_g=0.001, cfl=0.5),
     "C4": dict(kind="dune", n=16384, a_g=0.001, cfl=0.5),
+    "C4s": dict(kind="dune", n=4096, a_g=0.001, cfl=0.5),  # profiling size
     "C5": dict(kind="random", nx=8192, ny_per_gpu=4096, a_g=0.01, cfl=0.4),
 }
 

@@ -213,6 +213,12 @@ int silt_riemann_batch(const silt_problem* problem, const double* left,
                        const double* right, int64_t n, int axis, int variant,
                        double* out);
 
+/* Device math self-test (diagnostics): for k < n,
+ *   out[4k+0] = FAST reciprocal of x[k]      out[4k+1] = IEEE 1/x[k]
+ *   out[4k+2] = STRICT hypot(x[k], y[k])     out[4k+3] = FAST sqrt(x[k])
+ * Host arrays. */
+int silt_selftest_math(const double* x, const double* y, int64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,16 +48,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          extra: list[str] | None = None) -> str:
+    """Compile the library.  `out`/`extra` build an experimental variant
+    (e.g. a different register cap) next to the default one."""
+    lib = out or LIB
+    if out is None and not force and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    libdir = os.path.dirname(lib)
+    os.makedirs(libdir, exist_ok=True)
+    extra = extra or []
     objs = []
     procs = []
     for src, flags in UNITS:
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        obj = os.path.join(libdir, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC] + ARCH + COMMON + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + ARCH + COMMON + flags + extra + ["-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                             stderr=subprocess.STDOUT, text=True)))
     logs = []
@@ -67,16 +73,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.returncode != 0:
             sys.stderr.write(out)
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
+    with open(os.path.join(libdir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(logs))
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
+    cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs
     subprocess.run(cmd, check=True)
     for o in objs:
         os.remove(o)
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    out = None
+    extra = []
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    if "--extra" in args:
+        extra = args[args.index("--extra") + 1].split()
+    build(force="--force" in args, verbose=True, out=out, extra=extra)

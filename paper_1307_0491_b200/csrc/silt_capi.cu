@@ -706,4 +706,22 @@ int silt_riemann_batch(const silt_problem* problem, const double* left, const do
     return SILT_OK;
 }
 
+int silt_selftest_math(const double* x, const double* y, int64_t n, double* out) {
+    if (n <= 0) return SILT_OK;
+    CUDA_TRY(cudaSetDevice(0));
+    double *dx = nullptr, *dy = nullptr, *dout = nullptr;
+    CUDA_TRY(cudaMalloc(&dx, n * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dy, n * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dout, 4 * n * sizeof(double)));
+    cudaMemcpy(dx, x, n * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(dy, y, n * sizeof(double), cudaMemcpyHostToDevice);
+    silt_selftest_math_launch(dx, dy, n, dout);
+    cudaError_t e = cudaMemcpy(out, dout, 4 * n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dout);
+    if (e != cudaSuccess) return fail(SILT_ERR_CUDA, cudaGetErrorString(e));
+    return SILT_OK;
+}
+
 }  // extern "C"

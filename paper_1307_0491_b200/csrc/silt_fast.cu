@@ -3,3 +3,4 @@
 #include "silt_launch.h"
 
 SILT_DEFINE_LAUNCHERS(false, silt_fast)
+

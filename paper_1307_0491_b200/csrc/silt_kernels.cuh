@@ -9,12 +9,12 @@
 //   load state n (SoA, coalesced fp64) -> per-cell relaxation terms for the
 //   x and y axes (computed once, shared by both faces of the cell) ->
 //   x-face problem (right neighbour's terms by warp shuffle) -> x update ->
-//   y-face problem against the previous row (kept in registers) -> y update
-//   of the previous row -> check_depth -> store state n+1 -> CFL/hmax
+//   y-face problem against the previous row (kept in shared memory) -> y
+//   update of the previous row -> check_depth -> store state n+1 -> CFL/hmax
 //   candidates of state n+1 (the NEXT step's cfl_dt) folded into registers.
-// Each face is solved exactly once per launch (faces on strip seams by the
-// warp to their left... no: the x-halo lanes make every face belong to
-// exactly one warp), so depth and bed updates telescope exactly.
+// Every face is solved exactly once per launch: x faces by the lane left of
+// them (the halo lanes 0 and 31 make each x face belong to exactly one warp),
+// y faces by the owning column, so depth and bed updates telescope exactly.
 //
 // The run clock lives on the device (Control, triple-buffered per launch):
 // every CTA derives dt_n from the previous launch's reduced axis speeds and
@@ -279,10 +279,10 @@ __device__ __forceinline__ void cell_speeds(const StepArgs& A, const double c[4]
         double dqx = 0, dqy = 0, om;
         grass_terms_fast(P, u, v, s2, om, dqx);
         const double au = fabs(u), av = fabs(v);
-        sx = au + sqrt(smax(gh, fma(u, u, P.g * dqx)));
+        sx = au + fsqrt(smax(gh, fma(u, u, P.g * dqx)));
         if (A.dim == 2) {
             grass_terms_fast(P, v, u, s2, om, dqy);
-            sy = av + sqrt(smax(gh, fma(v, v, P.g * dqy)));
+            sy = av + fsqrt(smax(gh, fma(v, v, P.g * dqy)));
         } else {
             sy = 0.0;
         }
@@ -339,8 +339,11 @@ __device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4],
 }
 
 // ---- K1: fused 2D step ----------------------------------------------------
+#ifndef SILT_STEP_MIN_BLOCKS
+#define SILT_STEP_MIN_BLOCKS 2
+#endif------------------------------------------------
 template <bool S>
-__global__ void __launch_bounds__(kStepThreads) step2d_kernel(StepArgs A, int li) {
+__global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) control_epilogue(A, li, cur, d);

@@ -12,3 +12,5 @@
 
 SILT_DECLARE_LAUNCHERS(silt_fast)
 SILT_DECLARE_LAUNCHERS(silt_strict)
+
+void silt_selftest_math_launch(const double* x, const double* y, long long n, double* out);

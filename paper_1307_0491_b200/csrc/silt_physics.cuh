@@ -31,8 +31,56 @@ constexpr int kMaxNewton = 60;
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 
-// Round-to-nearest reciprocal (MUFU.RCP64H + Newton, IEEE-rounded).
-__device__ __forceinline__ double rcp(double y) { return __drcp_rn(y); }
+#ifndef SILT_RCP_FAST
+#define SILT_RCP_FAST 1
+#endif
+#ifndef SILT_FACE_TRY
+#define SILT_FACE_TRY 0
+#endif
+#ifndef SILT_SQRT_FAST
+#define SILT_SQRT_FAST 1
+#endif
+
+// Reciprocal for the FAST variant.  SILT_RCP_FAST: MUFU.RCP64H seed
+// (rcp.approx.ftz.f64) + one cubic Newton correction r += r(e + e^2),
+// e = 1 - y r: branch-free, within an ulp for normal, finite y (all uses here:
+// depths, celerities, Jacobian determinants).  Otherwise IEEE __drcp_rn.
+__device__ __forceinline__ double rcp(double y) {
+#if SILT_RCP_FAST
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    const double e = fma(-y, r, 1.0);
+    return fma(r, fma(e, e, e), r);
+#else
+    return __drcp_rn(y);
+#endif
+}
+
+// Square root for the FAST variant: MUFU.RSQ64H seed, two Newton steps on
+// y = 1/sqrt(x) and a final Markstein-style correction s = x y + y r / 2,
+// r = x - s0^2; branch-free for normal finite x >= 0 (x == 0 gives 0).
+__device__ __forceinline__ double fsqrt(double x) {
+#if SILT_SQRT_FAST
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    const double s0 = x * y;
+    const double r = fma(-s0, s0, x);
+    const double s = fma(0.5 * y, r, s0);
+    return x > 0.0 ? s : x;
+#else
+    return sqrt(x);
+#endif
+}
+
+template <bool S>
+__device__ __forceinline__ double dsqrt(double x) {
+    if constexpr (S)
+        return sqrt(x);
+    else
+        return fsqrt(x);
+}
 
 // glibc 2.39 hypot (sysdeps/ieee754/dbl-64/e_hypot.c, non-FMA kernel after
 // C. F. Borges, "An improved algorithm for hypot(a,b)", 2019), restated so the
@@ -129,7 +177,7 @@ __device__ __forceinline__ void grass_terms_fast(const Params& P, double un, dou
         dq = P.a_g * fma(3.0 * un, un, ut * ut);
         return;
     }
-    const double s = sqrt(s2);
+    const double s = fsqrt(s2);
     const double is = rcp(s);
     const double rate = grass_flux(s, P.a_g, P.m_g);
     const double drate = P.a_g * P.m_g * abs_pow(s, P.m_g - 1.0);
@@ -203,8 +251,8 @@ __device__ __forceinline__ CellPre cell_pre_fast(const Params& P, double h, doub
     c.v = c.wet ? hv * rh : 0.0;
     c.s2 = fma(c.u, c.u, c.v * c.v);
     c.pi = P.half_g * h * h;
-    c.tau = (h >= 1e-12) ? rh : 1e12;
-    c.sq = c.wet ? sqrt(P.g * h) : 0.0;
+    c.tau = (h < 1e-12) ? (1.0 / 1e-12) : rh;  // tau_of, src/riemann.cpp:50-52
+    c.sq = c.wet ? fsqrt(P.g * h) : 0.0;
     return c;
 }
 
@@ -353,8 +401,8 @@ __device__ __forceinline__ bool solve_solid_outer(const Side& l, const Side& r, 
     const double rad1 = tl * tl + 2.0 * k * dzl;
     const double rad4 = tr * tr + 2.0 * k * dzr;
     if (!(rad1 > 0) || !(rad4 > 0)) return false;
-    const double t1 = sqrt(rad1);
-    const double t4 = sqrt(rad4);
+    const double t1 = dsqrt<S>(rad1);
+    const double t4 = dsqrt<S>(rad4);
     const double u1 = m2 + b * t1;
     const double u4 = m4 - b * t4;
     const double p1 = kl - a * a * t1;
@@ -440,9 +488,20 @@ __device__ __forceinline__ double res_norm(const Eval& v) {
 }
 
 // solve_fluid_outer: src/riemann.cpp:152-262 (stopping rule of the code, :201-204)
-template <bool S>
-__device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, double a, double b,
-                                                  double g, Flux& F) {
+// Outcome of a branch solver attempt.
+constexpr int kIllPosed = 0;  // no positive fan at this celerity pair (IllPosed)
+constexpr int kSolved = 1;
+constexpr int kBail = 2;      // kTry only: leave it to the general solver
+
+// kTry = true is the inlined fast path: undamped Newton steps only, at most
+// kTryNewton of them; whenever the reference would backtrack, iterate longer
+// or enlarge, it bails out and the caller re-solves the face from scratch with
+// the general solver (same arithmetic, so the result is unchanged).
+constexpr int kTryNewton = 6;
+
+template <bool S, bool kTry = false>
+__device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, double a, double b,
+                                                 double g, Flux& F) {
     const double tl = l.tau, tr = r.tau;
     const double ul = l.un, ur = r.un;
     FluidCtx c;
@@ -485,7 +544,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
     double m4 = u0 + b * tsr;
 
     Eval e = fo_eval<S>(c, m2, m4);
-    if (!e.valid) return false;
+    if (!e.valid) return kTry ? kBail : kIllPosed;
 
     double tmax = tl;
     tmax = (tmax < tr) ? tr : tmax;
@@ -499,7 +558,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
 
     int it = 0;
     while (res_norm(e) > tol) {
-        if (++it > kMaxNewton) return false;
+        if (++it > (kTry ? kTryNewton : kMaxNewton)) return kTry ? kBail : kIllPosed;
         double j11, j12, j21, j22, det, step2, step4;
         if constexpr (S) {
             j11 = 2.0 * e.t1 / c.amb - c.kappa / b;
@@ -507,7 +566,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
             j21 = 2.0 * e.t1 / c.amb + e.t2 / b + 2.0 * c.k * e.dzl / e.d;
             j22 = -e.t2 / b + 2.0 * c.k * (c.jz - e.dzl) / e.d;
             det = j11 * j22 - j12 * j21;
-            if (det == 0.0 || !isfinite(det)) return false;
+            if (det == 0.0 || !isfinite(det)) return kTry ? kBail : kIllPosed;
             step2 = (e.r1 * j22 - e.r2 * j12) / det;
             step4 = (e.r2 * j11 - e.r1 * j21) / det;
         } else {
@@ -519,7 +578,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
             j21 = fma(e.t2, c.ib, fma(tk, e.dzl, t1a));
             j22 = fma(-e.t2, c.ib, tk * (c.jz - e.dzl));
             det = j11 * j22 - j12 * j21;
-            if (det == 0.0 || !isfinite(det)) return false;
+            if (det == 0.0 || !isfinite(det)) return kTry ? kBail : kIllPosed;
             const double idet = rcp(det);
             step2 = (e.r1 * j22 - e.r2 * j12) * idet;
             step4 = (e.r2 * j11 - e.r1 * j21) * idet;
@@ -527,7 +586,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
         double damp = 1.0;
         bool accepted = false;
         const double rn = res_norm(e);
-        for (int bt = 0; bt < 40; ++bt) {
+        for (int bt = 0; bt < (kTry ? 1 : 40); ++bt) {
             const Eval trial = fo_eval<S>(c, m2 - damp * step2, m4 - damp * step4);
             if (trial.valid && (res_norm(trial) < rn || res_norm(trial) <= tol)) {
                 m2 -= damp * step2;
@@ -538,7 +597,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
             }
             damp *= 0.5;
         }
-        if (!accepted) return false;
+        if (!accepted) return kTry ? kBail : kIllPosed;
     }
 
     const double ustar = 0.5 * (m2 + m4 - b * c.kappa);
@@ -557,7 +616,7 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
         default: hu = r.hun; uu = r.un; p = r.pi; w = r.omega; break;
     }
     publish(sp, ex, hu, uu, p, w, false, F);
-    return true;
+    return kSolved;
 }
 
 // interface_riemann (src/riemann.cpp:266-338) + the celerity pair of
@@ -565,12 +624,13 @@ __device__ __forceinline__ bool solve_fluid_outer(const Side& l, const Side& r, 
 // (src/stepper.cpp:87).  Returns false when no positive fan exists after
 // kMaxEnlarge enlargements (the reference throws runtime_error).
 template <bool S>
-__device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const Side& r, Flux& F) {
+__device__ __forceinline__ bool face_flux_general_impl(const Params& P, const Side& l, const Side& r,
+                                                       Flux& F) {
     F.h = F.huL = F.huR = F.hv = F.z = 0.0;
     if (!l.wet && !r.wet) return true;  // inert interface: a = b = 0
     const double a0 = P.safety * smax(smax(0.0, l.a_side), r.a_side);
     const double b0 =
-        (l.moving || r.moving) ? P.safety * sqrt(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
+        (l.moving || r.moving) ? P.safety * dsqrt<S>(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
     double a = a0, b = b0;
     bool ok = false;
     for (int attempt = 0; attempt <= kMaxEnlarge; ++attempt) {
@@ -586,7 +646,7 @@ __device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const 
         else if (be > ae)
             ok = solve_solid_outer<S>(l, r, ae, be, P.g, F);
         else
-            ok = solve_fluid_outer<S>(l, r, ae, be, P.g, F);
+            ok = solve_fluid_outer<S, false>(l, r, ae, be, P.g, F) == kSolved;
         if (ok) break;
         a *= 2.0;
         if (b > 0) b *= 2.0;
@@ -597,6 +657,41 @@ __device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const 
     }
     F.hv = F.h * (F.h > 0 ? l.ut : F.h < 0 ? r.ut : 0.0);
     return true;
+}
+
+// The general solver, out of line: every branch, the enlargement loop and
+// damped Newton.  Kept out of the hot loop's instruction stream.
+template <bool S>
+__device__ __noinline__ bool face_flux_general(const Params& P, const Side& l, const Side& r,
+                                               Flux& F) {
+    return face_flux_general_impl<S>(P, l, r, F);
+}
+
+// interface_riemann (src/riemann.cpp:266-338) + the celerity pair of
+// bounds_impl (src/relax_state.cpp:25-53) + the transverse flux of solve_face
+// (src/stepper.cpp:87).  Returns false when no positive fan exists after
+// kMaxEnlarge enlargements (the reference throws runtime_error).
+// Hot path inlined: the fluid-outer fan at the first celerity pair with full
+// Newton steps (100% of faces in C1/C3/C4/C5); anything else goes
+// to the out-of-line general solver, which recomputes the face from scratch.
+template <bool S>
+__device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const Side& r, Flux& F) {
+#if !SILT_FACE_TRY
+    return face_flux_general_impl<S>(P, l, r, F);
+#endif
+    if (l.wet || r.wet) {
+        const double a0 = P.safety * smax(smax(0.0, l.a_side), r.a_side);
+        const double b0 =
+            (l.moving || r.moving) ? P.safety * dsqrt<S>(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
+        if (b0 >= kSuppressB && a0 >= b0) {
+            const double ae = smax(a0, kGap * b0);
+            if (solve_fluid_outer<S, true>(l, r, ae, b0, P.g, F) == kSolved) {
+                F.hv = F.h * (F.h > 0 ? l.ut : F.h < 0 ? r.ut : 0.0);
+                return true;
+            }
+        }
+    }
+    return face_flux_general<S>(P, l, r, F);
 }
 
 // axis_speed: src/stepper.cpp:30-36 (STRICT, on primitives)

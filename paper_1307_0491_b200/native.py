@@ -16,7 +16,8 @@ import numpy as np
 from . import abi
 from .abi import SiltExchange, SiltProblem, SiltRunPlan, SiltStatus, SiltStrip
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsilt_b200.so")
+LIB_PATH = os.environ.get(
+    "SILT_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsilt_b200.so"))
 
 
 class SiltLibraryMissing(ImportError):
@@ -79,6 +80,7 @@ def lib() -> C.CDLL:
         "silt_cfl_dt": ([_P, _D, C.c_int, _D], C.c_int),
         "silt_step_padded": ([_P, _D, C.c_double, C.c_int], C.c_int),
         "silt_riemann_batch": ([_P, _D, _D, C.c_int64, C.c_int, C.c_int, _D], C.c_int),
+        "silt_selftest_math": ([_D, _D, C.c_int64, _D], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -263,4 +265,13 @@ def faces(problem: SiltProblem, left: np.ndarray, right: np.ndarray, axis: int,
     out = np.empty((left.shape[0], 5))
     check(lib().silt_riemann_batch(C.byref(problem), _dp(left), _dp(right), left.shape[0],
                                    axis, variant, _dp(out)))
+    return out
+
+
+def selftest_math(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """(n, 4): fast rcp, IEEE rcp, strict (glibc) hypot, sqrt — on the device."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.empty((x.size, 4))
+    check(lib().silt_selftest_math(_dp(x), _dp(y), x.size, _dp(out)))
     return out

@@ -31,6 +31,7 @@ class Backend:
     """Adapter: run / cfl_dt / step_padded / faces + error classification."""
 
     name = "?"
+    bitwise = True  # reproduces the reference's rounding (STRICT / checkers)
 
     def run(self, p, init, *, t_end=math.inf, max_steps=-1, snapshots=()):
         raise NotImplementedError
@@ -231,7 +232,14 @@ def kat_extruded(b: Backend):
     pd[-1, 1:-1] = two[0]
     c = b.step_padded(p2, pd, dt)
     for j in range(ny):
-        assert np.array_equal(c[j + 1, 1:-1], a[1, 1:-1])
+        if b.bitwise:
+            assert np.array_equal(c[j + 1, 1:-1], a[1, 1:-1])
+        else:
+            # FMA-contracted arithmetic: the mirror-symmetric y fans leave a
+            # rounding-level exchange residue in hv
+            d = np.abs(c[j + 1, 1:-1] - a[1, 1:-1])
+            assert np.all(d[:, [0, 1, 3]] <= 1e-13 * np.abs(a[1, 1:-1, [0, 1, 3]]).T.max(0))
+            assert np.all(d[:, 2] <= 1e-13)
 
 
 def kat_y_symmetry(b: Backend):
