@@ -340,7 +340,7 @@ __device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4],
 
 // ---- K1: fused 2D step ----------------------------------------------------
 #ifndef SILT_STEP_MIN_BLOCKS
-#define SILT_STEP_MIN_BLOCKS 2
+#define SILT_STEP_MIN_BLOCKS 3
 #endif------------------------------------------------
 template <bool S>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {

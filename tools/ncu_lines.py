@@ -53,7 +53,7 @@ def sass_lines(lib: str, kernel_mangled_part: str, tu: str):
                 if m:
                     cur = f"{os.path.basename(m.group(1))}:{m.group(2)}"
                     continue
-                if re.search(r"/\*[0-9a-f]{4}\*/", line):
+                if re.search(r"/\*[0-9a-f]{4,}\*/", line):
                     out.append(cur)
             return out
     raise SystemExit("kernel not found in cubin")
