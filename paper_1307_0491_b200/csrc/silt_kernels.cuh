@@ -341,9 +341,108 @@ __device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4],
 // ---- K1: fused 2D step ----------------------------------------------------
 #ifndef SILT_STEP_MIN_BLOCKS
 #define SILT_STEP_MIN_BLOCKS 3
-#endif------------------------------------------------
+#endif
+
+// Source of one field of cell (col, row) for the cp.async row prefetch: the
+// interior plane, a ghost-row buffer, a caller-given ghost column, or the
+// interior cell a physical x-boundary ghost is derived from (fixed up after
+// the copy lands, see fix_xghost).
+__device__ __forceinline__ const double* cell_src(const StepArgs& A, int p, int col, int row,
+                                                  int f) {
+    const int nx = A.nx;
+    if (row < 0 || row >= A.ny) {
+        const double* g;
+        if (row < 0)
+            g = A.south_nbr ? A.recv_s : A.ghost_s[p];
+        else
+            g = A.north_nbr ? A.recv_n : A.ghost_n[p];
+        return g + (size_t)f * nx + min(max(col, 0), nx - 1);
+    }
+    int c;
+    if (col == -1 || col == nx) {
+        const int side = col < 0 ? SILT_WEST : SILT_EAST;
+        const int t = A.bc_type[side];
+        if (t == SILT_BC_GIVEN)
+            return (side == SILT_WEST ? A.ghost_w : A.ghost_e) + (size_t)f * A.ny + row;
+        if (t == SILT_BC_PERIODIC)
+            c = col < 0 ? nx - 1 : 0;
+        else
+            c = col < 0 ? 0 : nx - 1;
+    } else {
+        c = min(max(col, 0), nx - 1);  // dead lanes: any valid cell
+    }
+    return A.state[p][f] + (size_t)row * A.pitch + c;
+}
+
+// Physical x-boundary ghost (apply_bc_side, src/scenarios.cpp:78-99) applied
+// to the interior cell copied by cell_src.
+__device__ __forceinline__ void fix_xghost(const StepArgs& A, int col, int row, double c[4]) {
+    if (row < 0 || row >= A.ny || (col != -1 && col != A.nx)) return;
+    const int side = col < 0 ? SILT_WEST : SILT_EAST;
+    const int t = A.bc_type[side];
+    if (t == SILT_BC_GIVEN || t == SILT_BC_PERIODIC) return;
+    ghost_transform(A, side, c);
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+__device__ __forceinline__ void side_to_ring(double (*ring)[kStepThreads], const Side& s, int lane) {
+    ring[0][lane] = s.h;
+    ring[1][lane] = s.hun;
+    ring[2][lane] = s.pi;
+    ring[3][lane] = s.z;
+    ring[4][lane] = s.omega;
+    ring[5][lane] = s.un;
+    ring[6][lane] = s.ut;
+    ring[7][lane] = s.tau;
+    ring[8][lane] = s.a_side;
+    ring[9][lane] = s.b2_side;
+    ring[10][lane] = __hiloint2double(0, s.wet | (s.moving << 1));
+}
+
+__device__ __forceinline__ Side side_from_ring(const double (*ring)[kStepThreads], int lane) {
+    Side s;
+    s.h = ring[0][lane];
+    s.hun = ring[1][lane];
+    s.pi = ring[2][lane];
+    s.z = ring[3][lane];
+    s.omega = ring[4][lane];
+    s.un = ring[5][lane];
+    s.ut = ring[6][lane];
+    s.tau = ring[7][lane];
+    s.a_side = ring[8][lane];
+    s.b2_side = ring[9][lane];
+    const int fl = __double2loint(ring[10][lane]);
+    s.wet = fl & 1;
+    s.moving = (fl >> 1) & 1;
+    return s;
+}
+
+template <bool S>
+__device__ __forceinline__ Side side_of(const StepArgs& A, const double c[4], bool xaxis) {
+    if constexpr (S) {
+        return xaxis ? make_side_ref(A.P, c[0], c[1], c[2], c[3])
+                     : make_side_ref(A.P, c[0], c[2], c[1], c[3]);
+    } else {
+        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
+        return make_side_fast(A.P, pre, xaxis);
+    }
+}
+
 template <bool S>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
+    // Per-thread march state in shared memory (SoA by thread: conflict-free),
+    // so that registers at each face solve hold little beyond the solver.
+    __shared__ double sh_side[11][kStepThreads];   // y-side terms of row r-1
+    __shared__ double sh_xs[4][kStepThreads];      // x-updated row r-1
+    __shared__ double sh_fy[4][kStepThreads];      // y face below row r-1: h, huR, hv, z
+    __shared__ double sh_row[2][4][kStepThreads];  // cp.async row prefetch
+
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) control_epilogue(A, li, cur, d);
@@ -351,8 +450,9 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     Slot& nxt = A.ctl->slot[(li + 1) % 3];
 
     const int p = (int)(cur.steps & 1), q = p ^ 1;
-    const int lane = threadIdx.x & 31;
-    const int strip = blockIdx.x * (kStepThreads / 32) + (threadIdx.x >> 5);
+    const int t = threadIdx.x;
+    const int lane = t & 31;
+    const int strip = blockIdx.x * (kStepThreads / 32) + (t >> 5);
     const int i0 = strip * kCellsPerWarp;
     if (i0 >= A.nx) return;  // warp-uniform
     const int col = i0 - 1 + lane;
@@ -364,80 +464,82 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const double cx = d.dt / A.dx;
     const double cy = d.dt / A.dy;
     const double href = __longlong_as_double((long long)cur.hmax);
+    double(*side_prev)[kStepThreads] = sh_side;
 
     Reduce R{0.0, 0.0, 0.0, 0u};
-    Side yprev;
-    double xs_prev[4] = {0, 0, 0, 0};
-    Flux fy_prev{0, 0, 0, 0, 0};
-    bool fail_riemann = false;
-
-    double c[4];
-    load_cell(A, p, col, jb - 1, c);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) cp_async8(&sh_row[0][f][t], cell_src(A, p, col, jb - 1, f));
+    cp_async_commit();
+    int buf = 0;
+#pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
-        double cn[4];
-        if (r < je) load_cell(A, p, col, r + 1, cn);  // prefetch next row
-        const bool own_row = r >= jb && r < je;
-        Side sx, sy;
-        make_sides<S>(A, c, sx, sy, own_row);
-        double xs[4] = {c[0], c[1], c[2], c[3]};
-        if (own_row) {
-            // x faces: this lane solves the face between col and col+1
-            const Side right = shfl_down_side(sx);
-            Flux fx{0, 0, 0, 0, 0};
-            if (xface) {
-                if (!face_flux<S>(A.P, sx, right, fx)) {
-                    const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
-                    record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
-                    fail_riemann = true;
-                }
-            }
-            const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
-            const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
-            // x update (step_2d x sweep, src/stepper.cpp:165-170)
-            xs[0] = c[0] - cx * (fx.h - lh);
-            xs[1] = c[1] - cx * (fx.huL - lhuR);
-            xs[2] = c[2] - cx * (fx.hv - lhv);
-            xs[3] = c[3] - cx * (fx.z - lz);
-        }
-        if (r > jb - 1) {
-            // y face between rows r-1 and r (normal = v, transverse = u)
-            Flux fy{0, 0, 0, 0, 0};
-            if (owned) {
-                if (!face_flux<S>(A.P, yprev, sy, fy)) {
-                    const double info[6] = {yprev.h, yprev.un, yprev.z, sy.h, sy.un, sy.z};
-                    record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
-                    fail_riemann = true;
-                }
-            }
-            if (r - 1 >= jb && owned) {
-                // y update of row r-1 (src/stepper.cpp:181-186) + check_depth
-                double o[4];
-                o[0] = xs_prev[0] - cy * (fy.h - fy_prev.h);
-                o[2] = xs_prev[2] - cy * (fy.huL - fy_prev.huR);
-                o[1] = xs_prev[1] - cy * (fy.hv - fy_prev.hv);
-                o[3] = xs_prev[3] - cy * (fy.z - fy_prev.z);
-                if (!check_depth(o[0], href)) {
-                    record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
-                }
-                const size_t off = (size_t)(r - 1) * A.pitch + col;
-#pragma unroll
-                for (int f = 0; f < 4; ++f) A.state[q][f][off] = o[f];
-                write_edges(A, q, col, r - 1, o);
-                double ssx, ssy;
-                cell_speeds<S>(A, o, ssx, ssy);
-                reduce_fold(A, R, o, ssx, ssy);
-            }
-            fy_prev = fy;
-        }
-        yprev = sy;
-#pragma unroll
-        for (int f = 0; f < 4; ++f) xs_prev[f] = xs[f];
         if (r < je) {
 #pragma unroll
-            for (int f = 0; f < 4; ++f) c[f] = cn[f];
+            for (int f = 0; f < 4; ++f)
+                cp_async8(&sh_row[buf ^ 1][f][t], cell_src(A, p, col, r + 1, f));
         }
+        cp_async_commit();
+        cp_async_wait1();
+        double c[4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) c[f] = sh_row[buf][f][t];
+        buf ^= 1;
+        fix_xghost(A, col, r, c);
+        const bool own_row = r >= jb && r < je;
+
+        // y face between rows r-1 and r (normal = v, transverse = u), solved
+        // first so that only this row's x-side is carried across it
+        Flux fy{0, 0, 0, 0, 0};
+        {
+            const Side sy = side_of<S>(A, c, false);
+            if (r > jb - 1 && owned) {
+                const Side lo = side_from_ring(side_prev, t);
+                if (!face_flux<S>(A.P, lo, sy, fy)) {
+                    const double info[6] = {lo.h, lo.un, lo.z, sy.h, sy.un, sy.z};
+                    record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
+                }
+            }
+            side_to_ring(side_prev, sy, t);
+        }
+        if (r - 1 >= jb && owned) {
+            // y update of row r-1 (src/stepper.cpp:181-186) + check_depth
+            double o[4];
+            o[0] = sh_xs[0][t] - cy * (fy.h - sh_fy[0][t]);
+            o[2] = sh_xs[2][t] - cy * (fy.huL - sh_fy[1][t]);
+            o[1] = sh_xs[1][t] - cy * (fy.hv - sh_fy[2][t]);
+            o[3] = sh_xs[3][t] - cy * (fy.z - sh_fy[3][t]);
+            if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
+            const size_t off = (size_t)(r - 1) * A.pitch + col;
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.state[q][f][off] = o[f];
+            write_edges(A, q, col, r - 1, o);
+            double ssx, ssy;
+            cell_speeds<S>(A, o, ssx, ssy);
+            reduce_fold(A, R, o, ssx, ssy);
+        }
+        if (!own_row) continue;  // warp-uniform
+        sh_fy[0][t] = fy.h;
+        sh_fy[1][t] = fy.huR;
+        sh_fy[2][t] = fy.hv;
+        sh_fy[3][t] = fy.z;
+        // x faces: this lane solves the face between col and col+1
+        Flux fx{0, 0, 0, 0, 0};
+        {
+            const Side sx = side_of<S>(A, c, true);
+            const Side right = shfl_down_side(sx);
+            if (xface && !face_flux<S>(A.P, sx, right, fx)) {
+                const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
+                record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
+            }
+        }
+        const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
+        const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
+        // x update (step_2d x sweep, src/stepper.cpp:165-170)
+        sh_xs[0][t] = c[0] - cx * (fx.h - lh);
+        sh_xs[1][t] = c[1] - cx * (fx.huL - lhuR);
+        sh_xs[2][t] = c[2] - cx * (fx.hv - lhv);
+        sh_xs[3][t] = c[3] - cx * (fx.z - lz);
     }
-    (void)fail_riemann;
     reduce_flush(R, nxt);
 }
 

@@ -34,9 +34,6 @@ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b 
 #ifndef SILT_RCP_FAST
 #define SILT_RCP_FAST 1
 #endif
-#ifndef SILT_FACE_TRY
-#define SILT_FACE_TRY 0
-#endif
 #ifndef SILT_SQRT_FAST
 #define SILT_SQRT_FAST 1
 #endif
@@ -493,10 +490,10 @@ constexpr int kIllPosed = 0;  // no positive fan at this celerity pair (IllPosed
 constexpr int kSolved = 1;
 constexpr int kBail = 2;      // kTry only: leave it to the general solver
 
-// kTry = true is the inlined fast path: undamped Newton steps only, at most
-// kTryNewton of them; whenever the reference would backtrack, iterate longer
-// or enlarge, it bails out and the caller re-solves the face from scratch with
-// the general solver (same arithmetic, so the result is unchanged).
+// kTry = true: undamped Newton steps only, at most kTryNewton of them; the
+// caller re-solves from scratch with kTry = false when it bails out (same
+// arithmetic, same result).  Measured slower than the plain solver on sm_100a
+// (out-of-line fallback costs registers), so the step kernels use kTry = false.
 constexpr int kTryNewton = 6;
 
 template <bool S, bool kTry = false>
@@ -659,39 +656,13 @@ __device__ __forceinline__ bool face_flux_general_impl(const Params& P, const Si
     return true;
 }
 
-// The general solver, out of line: every branch, the enlargement loop and
-// damped Newton.  Kept out of the hot loop's instruction stream.
-template <bool S>
-__device__ __noinline__ bool face_flux_general(const Params& P, const Side& l, const Side& r,
-                                               Flux& F) {
-    return face_flux_general_impl<S>(P, l, r, F);
-}
-
 // interface_riemann (src/riemann.cpp:266-338) + the celerity pair of
 // bounds_impl (src/relax_state.cpp:25-53) + the transverse flux of solve_face
 // (src/stepper.cpp:87).  Returns false when no positive fan exists after
 // kMaxEnlarge enlargements (the reference throws runtime_error).
-// Hot path inlined: the fluid-outer fan at the first celerity pair with full
-// Newton steps (100% of faces in C1/C3/C4/C5); anything else goes
-// to the out-of-line general solver, which recomputes the face from scratch.
 template <bool S>
 __device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const Side& r, Flux& F) {
-#if !SILT_FACE_TRY
     return face_flux_general_impl<S>(P, l, r, F);
-#endif
-    if (l.wet || r.wet) {
-        const double a0 = P.safety * smax(smax(0.0, l.a_side), r.a_side);
-        const double b0 =
-            (l.moving || r.moving) ? P.safety * dsqrt<S>(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
-        if (b0 >= kSuppressB && a0 >= b0) {
-            const double ae = smax(a0, kGap * b0);
-            if (solve_fluid_outer<S, true>(l, r, ae, b0, P.g, F) == kSolved) {
-                F.hv = F.h * (F.h > 0 ? l.ut : F.h < 0 ? r.ut : 0.0);
-                return true;
-            }
-        }
-    }
-    return face_flux_general<S>(P, l, r, F);
 }
 
 // axis_speed: src/stepper.cpp:30-36 (STRICT, on primitives)
