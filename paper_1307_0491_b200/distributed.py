@@ -252,3 +252,108 @@ class StripRunner:
     def shutdown(self):
         if self._dist is not None and self._dist.is_initialized():
             self._dist.destroy_process_group()
+
+
+class LocalStripGroup:
+    """run_parallel(sc, 1, py) in ONE process (src/parallel.cpp:261-386): py
+    row strips, strip k on CUDA device ``devices[k % len(devices)]``, all
+    enqueued on per-device streams in lock step.  Ghost rows move with device
+    (or peer) copies and the axis-speed maxima are reduced on device, so the
+    per-step device protocol is exactly the one the NCCL driver runs.
+    """
+
+    def __init__(self, problem, py: int, devices=(0,), variant: int = abi.VARIANT_FAST):
+        import torch
+        from . import native
+        ny = 1 if problem.dim == 1 else problem.ny
+        if py < 1 or py > ny:
+            raise ValueError("partition: every worker needs at least one cell per axis")
+        if problem.dim == 1 and py != 1:
+            raise ValueError("partition: 1D grids require py == 1")
+        self.problem, self.py = problem, py
+        periodic_y = problem.dim == 2 and problem.bc[abi.SOUTH].type == abi.BC_PERIODIC
+        self.strips = []
+        for r in range(py):
+            j0, n = block_range(ny, py, r)
+            south, north = neighbours(r, py, periodic_y)
+            dev = devices[r % len(devices)]
+            st = abi.SiltStrip(j0, n, int(south is not None), int(north is not None))
+            s = native.Solver(problem, st, dev, variant)
+            stream = torch.cuda.Stream(device=dev)
+            s.set_stream(stream.cuda_stream)
+            ex = s.exchange_ptrs()
+            d = torch.device("cuda", dev)
+            wrap = (lambda ptr, n=ex.row_doubles, d=d:
+                    torch.as_tensor(_CAI(ptr, n), device=d) if ptr else None)
+            self.strips.append(dict(solver=s, stream=stream, device=d, j0=j0, n=n,
+                                    south=south, north=north,
+                                    send_s=wrap(ex.send_south), send_n=wrap(ex.send_north),
+                                    recv_s=wrap(ex.recv_south), recv_n=wrap(ex.recv_north)))
+
+    def _sync_streams(self):
+        for s in self.strips:
+            s["stream"].synchronize()
+
+    def _exchange(self):
+        import torch
+        if self.py == 1:
+            return
+        self._sync_streams()
+        with torch.no_grad():
+            for s in self.strips:
+                if s["south"] is not None:
+                    src = self.strips[s["south"]]
+                    s["recv_s"].copy_(src["send_n"])
+                if s["north"] is not None:
+                    src = self.strips[s["north"]]
+                    s["recv_n"].copy_(src["send_s"])
+            slots = [torch.as_tensor(_CAI(s["solver"].reduce_slot(), 2), device=s["device"])
+                     for s in self.strips]
+            m = slots[0].clone()
+            for t in slots[1:]:
+                m = torch.maximum(m, t.to(m.device))
+            for t in slots:
+                t.copy_(m.to(t.device))
+        torch.cuda.synchronize()
+
+    def upload(self, field: np.ndarray):
+        for s in self.strips:
+            s["solver"].upload(np.ascontiguousarray(field[s["j0"]:s["j0"] + s["n"]]))
+
+    def begin(self, t_end: float = np.inf, max_steps: int = -1, snapshots=(), dt_cap: int = 0):
+        for s in self.strips:
+            s["solver"].begin(t_end=t_end, max_steps=max_steps, snapshots=snapshots, dt_cap=dt_cap)
+        self._exchange()
+
+    def step(self, n: int = 1):
+        for _ in range(n):
+            for s in self.strips:
+                s["solver"].step(1)
+            self._exchange()
+
+    def status(self):
+        sts = [s["solver"].status() for s in self.strips]
+        return sts[0]
+
+    def resume(self):
+        for s in self.strips:
+            s["solver"].resume()
+
+    def gather(self) -> np.ndarray:
+        return np.concatenate([s["solver"].download() for s in self.strips], axis=0)
+
+    def run(self, batch: int = 8, on_snapshot=None):
+        while True:
+            self.step(batch)
+            st = self.status()
+            if st.state == abi.STATE_PAUSED:
+                if on_snapshot is not None:
+                    on_snapshot(st.t, self.gather())
+                self.resume()
+                continue
+            if st.state == abi.STATE_DONE:
+                return st
+
+    def close(self):
+        for s in self.strips:
+            s["solver"].close()

@@ -204,3 +204,30 @@ def test_device_math(N):
     assert np.array_equal(out[:, 1], 1.0 / ax)
     assert np.all(np.abs(out[:, 0] - 1.0 / ax) <= np.spacing(1.0 / ax))
     assert np.all(np.abs(out[:, 3] - np.sqrt(ax)) <= np.spacing(np.sqrt(ax)))
+
+
+@pytest.mark.parametrize("py", [2, 3, 5])
+@pytest.mark.parametrize("case", ["rand48x32", "bc_periodic", "bc_inflow_wall"])
+def test_strip_group_bitwise(N, golden, case, py):
+    """Row strips on one GPU through the multi-strip device protocol (send /
+    recv rows, MAX-reduced speed slots, per-strip hmax): STRICT equals the
+    reference bit for bit for every layout (tests/test_parallel.cpp:215-238)."""
+    from paper_1307_0491_b200.distributed import LocalStripGroup
+    data, meta = golden
+    m = meta["cases"][case]
+    p = problem_from_meta(m)
+    for variant in (abi.VARIANT_STRICT, abi.VARIANT_FAST):
+        g = LocalStripGroup(p, py, devices=(0,), variant=variant)
+        g.upload(data[f"{case}_init"])
+        g.begin(max_steps=m["max_steps"], snapshots=m["snapshots"])
+        seen = []
+        st = g.run(batch=5, on_snapshot=lambda t, f: seen.append(t))
+        out = g.gather()
+        g.close()
+        assert st.steps == m["steps"]
+        assert seen == [s for s in m["snapshots"] if s <= m["t_final"]]
+        if variant == abi.VARIANT_STRICT:
+            assert st.t == m["t_final"]
+            assert np.array_equal(out, data[f"{case}_final"])
+        else:
+            assert np.all(normwise(out, data[f"{case}_final"]) <= FIELD_TOL)
