@@ -165,8 +165,9 @@ class StripRunner:
     def upload_host(self, array):
         if hasattr(array, "data_ptr"):
             import ctypes as C
-            self.solver.L.silt_solver_upload(self.solver.h,
-                                             C.cast(array.data_ptr(), C.POINTER(C.c_double)))
+            from .native import check
+            check(self.solver.L.silt_solver_upload(self.solver.h,
+                                                   C.cast(array.data_ptr(), C.POINTER(C.c_double))))
         else:
             self.solver.upload(array)
 
