@@ -194,6 +194,25 @@ int silt_solver_exchange_ptrs(silt_solver* s, silt_exchange* out);
 /* Number of kernel launches this handle has enqueued (for accounting). */
 int silt_solver_launch_count(silt_solver* s, int64_t* count);
 
+/* ---- in-process strip group: run_parallel(sc, 1, py) ---------------------
+ * py row strips (block_range partition, src/parallel.cpp:25-30) in one
+ * process, strip k on devices[k % n_devices].  Per step, with no host
+ * synchronisation: the step kernels, ghost rows moved by device/peer copies
+ * and the axis-speed maxima reduced on devices[0] (stream events order the
+ * cross-device traffic).  Replaces run_parallel (src/parallel.cpp:261-386). */
+typedef struct silt_group silt_group;
+int silt_group_create(const silt_problem* problem, int py, const int* devices, int n_devices,
+                      int variant, silt_group** out);
+int silt_group_destroy(silt_group* g);
+/* whole-grid AoS field (nx * ny cells) */
+int silt_group_upload(silt_group* g, const double* host_aos);
+int silt_group_download(silt_group* g, double* host_aos);
+int silt_group_begin(silt_group* g, const silt_run_plan* plan);
+int silt_group_step(silt_group* g, int n);
+int silt_group_status(silt_group* g, silt_status* st);
+int silt_group_resume(silt_group* g);
+int silt_group_dt_log(silt_group* g, double* host_out, int64_t n);
+
 /* ---- one-shot conveniences (mirror the reference free functions) ---------- */
 /* run_serial: whole run on one GPU; host AoS in/out; dt_log may be NULL. */
 int silt_run(const silt_problem* problem, const double* init_aos,

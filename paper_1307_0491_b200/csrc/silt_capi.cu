@@ -578,6 +578,232 @@ int silt_solver_launch_count(silt_solver* s, int64_t* count) {
     return SILT_OK;
 }
 
+}  // extern "C"
+
+// ---- strip group --------------------------------------------------------------
+namespace {
+
+__global__ void max_slots_kernel(const double* gathered, int n, double* result) {
+    double sx = 0.0, sy = 0.0;
+    for (int k = 0; k < n; ++k) {
+        sx = gathered[2 * k] > sx ? gathered[2 * k] : sx;
+        sy = gathered[2 * k + 1] > sy ? gathered[2 * k + 1] : sy;
+    }
+    result[0] = sx;
+    result[1] = sy;
+}
+
+void block_range(int n, int parts, int r, int* offset, int* count) {
+    const int base = n / parts, rem = n % parts;
+    *count = base + (r < rem ? 1 : 0);
+    *offset = r * base + std::min(r, rem);
+}
+
+}  // namespace
+
+struct silt_group {
+    std::vector<silt_solver*> strips;
+    std::vector<int> south, north;   // neighbour strip or -1
+    std::vector<cudaEvent_t> stepped, copied;
+    int dev0 = 0;
+    double* gathered = nullptr;      // on dev0: [py][2]
+    double* result = nullptr;        // on dev0: [2]
+    cudaStream_t s0 = nullptr;       // reduction stream on dev0
+    cudaEvent_t reduced = nullptr;
+    int nx = 0, ny = 0;
+};
+
+namespace {
+
+int group_exchange(silt_group* g) {
+    const int py = (int)g->strips.size();
+    if (py == 1) return SILT_OK;
+    // 1. every strip finished its step
+    for (int k = 0; k < py; ++k) {
+        CUDA_TRY(cudaSetDevice(g->strips[k]->device));
+        CUDA_TRY(cudaEventRecord(g->stepped[k], g->strips[k]->stream));
+    }
+    // 2. gather the slots on dev0, MAX, scatter back
+    CUDA_TRY(cudaSetDevice(g->dev0));
+    for (int k = 0; k < py; ++k) {
+        CUDA_TRY(cudaStreamWaitEvent(g->s0, g->stepped[k], 0));
+        const Slot* slot = &g->strips[k]->ctl->slot[g->strips[k]->launches % 3];
+        CUDA_TRY(cudaMemcpyAsync(g->gathered + 2 * k, &slot->max_sx, 2 * sizeof(double),
+                                 cudaMemcpyDefault, g->s0));
+    }
+    max_slots_kernel<<<1, 1, 0, g->s0>>>(g->gathered, py, g->result);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(g->reduced, g->s0));
+    // 3. per strip: reduced maxima + ghost rows from the neighbours' send rows
+    const size_t row = 4 * (size_t)g->nx * sizeof(double);
+    for (int k = 0; k < py; ++k) {
+        silt_solver* s = g->strips[k];
+        CUDA_TRY(cudaSetDevice(s->device));
+        CUDA_TRY(cudaStreamWaitEvent(s->stream, g->reduced, 0));
+        Slot* slot = &s->ctl->slot[s->launches % 3];
+        CUDA_TRY(cudaMemcpyAsync(&slot->max_sx, g->result, 2 * sizeof(double), cudaMemcpyDefault,
+                                 s->stream));
+        if (g->south[k] >= 0) {
+            silt_solver* src = g->strips[g->south[k]];
+            CUDA_TRY(cudaStreamWaitEvent(s->stream, g->stepped[g->south[k]], 0));
+            CUDA_TRY(cudaMemcpyAsync(s->args.recv_s, src->args.send_n, row, cudaMemcpyDefault,
+                                     s->stream));
+        }
+        if (g->north[k] >= 0) {
+            silt_solver* src = g->strips[g->north[k]];
+            CUDA_TRY(cudaStreamWaitEvent(s->stream, g->stepped[g->north[k]], 0));
+            CUDA_TRY(cudaMemcpyAsync(s->args.recv_n, src->args.send_s, row, cudaMemcpyDefault,
+                                     s->stream));
+        }
+        CUDA_TRY(cudaEventRecord(g->copied[k], s->stream));
+    }
+    // 4. a strip's next step overwrites its send rows: wait for the readers
+    for (int k = 0; k < py; ++k) {
+        silt_solver* s = g->strips[k];
+        CUDA_TRY(cudaSetDevice(s->device));
+        if (g->south[k] >= 0) CUDA_TRY(cudaStreamWaitEvent(s->stream, g->copied[g->south[k]], 0));
+        if (g->north[k] >= 0) CUDA_TRY(cudaStreamWaitEvent(s->stream, g->copied[g->north[k]], 0));
+    }
+    return SILT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int silt_group_destroy(silt_group* g) {
+    if (!g) return SILT_OK;
+    for (silt_solver* s : g->strips) silt_solver_destroy(s);
+    cudaSetDevice(g->dev0);
+    if (g->s0) cudaStreamSynchronize(g->s0);
+    for (auto e : g->stepped) cudaEventDestroy(e);
+    for (auto e : g->copied) cudaEventDestroy(e);
+    if (g->reduced) cudaEventDestroy(g->reduced);
+    if (g->s0) cudaStreamDestroy(g->s0);
+    cudaFree(g->gathered);
+    cudaFree(g->result);
+    delete g;
+    return SILT_OK;
+}
+
+int silt_group_create(const silt_problem* problem, int py, const int* devices, int n_devices,
+                      int variant, silt_group** out) {
+    if (!out) return fail(SILT_ERR_INVALID, "silt_group_create: null out");
+    *out = nullptr;
+    if (int rc = validate_problem(problem)) return rc;
+    const int ny = problem->dim == 1 ? 1 : problem->ny;
+    if (py < 1) return fail(SILT_ERR_INVALID, "partition: worker counts must be >= 1");
+    if (problem->dim == 1 && py != 1) return fail(SILT_ERR_INVALID, "partition: 1D grids require py == 1");
+    if (py > ny) return fail(SILT_ERR_INVALID, "partition: every worker needs at least one cell per axis");
+    const int dev_default = 0;
+    if (n_devices < 1 || !devices) {
+        devices = &dev_default;
+        n_devices = 1;
+    }
+    silt_group* g = new silt_group();
+    g->nx = problem->nx;
+    g->ny = ny;
+    g->dev0 = devices[0];
+    const bool per_y = problem->dim == 2 && problem->bc[SILT_SOUTH].type == SILT_BC_PERIODIC;
+    for (int k = 0; k < py; ++k) {
+        int j0, n;
+        block_range(ny, py, k, &j0, &n);
+        const int south = k > 0 ? k - 1 : (per_y && py > 1 ? py - 1 : -1);
+        const int north = k < py - 1 ? k + 1 : (per_y && py > 1 ? 0 : -1);
+        silt_strip st{j0, n, south >= 0, north >= 0};
+        silt_solver* s = nullptr;
+        if (int rc = silt_solver_create(problem, &st, devices[k % n_devices], variant, &s)) {
+            silt_group_destroy(g);
+            return rc;
+        }
+        g->strips.push_back(s);
+        g->south.push_back(south);
+        g->north.push_back(north);
+        cudaEvent_t e1, e2;
+        cudaSetDevice(s->device);
+        cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e2, cudaEventDisableTiming);
+        g->stepped.push_back(e1);
+        g->copied.push_back(e2);
+    }
+    cudaSetDevice(g->dev0);
+    if (cudaStreamCreateWithFlags(&g->s0, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->reduced, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&g->gathered, 2 * py * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&g->result, 2 * sizeof(double)) != cudaSuccess) {
+        silt_group_destroy(g);
+        return fail(SILT_ERR_CUDA, "silt_group_create: allocation failed");
+    }
+    *out = g;
+    return SILT_OK;
+}
+
+int silt_group_upload(silt_group* g, const double* host_aos) {
+    if (!g || !host_aos) return fail(SILT_ERR_INVALID, "silt_group_upload: null argument");
+    for (silt_solver* s : g->strips)
+        if (int rc = silt_solver_upload(s, host_aos + 4 * (size_t)s->strip.j0 * g->nx)) return rc;
+    return SILT_OK;
+}
+
+int silt_group_download(silt_group* g, double* host_aos) {
+    if (!g || !host_aos) return fail(SILT_ERR_INVALID, "silt_group_download: null argument");
+    for (silt_solver* s : g->strips)
+        if (int rc = silt_solver_download(s, host_aos + 4 * (size_t)s->strip.j0 * g->nx)) return rc;
+    return SILT_OK;
+}
+
+int silt_group_begin(silt_group* g, const silt_run_plan* plan) {
+    if (!g) return fail(SILT_ERR_INVALID, "null group");
+    for (silt_solver* s : g->strips)
+        if (int rc = silt_solver_begin(s, plan)) return rc;
+    return group_exchange(g);
+}
+
+int silt_group_step(silt_group* g, int n) {
+    if (!g) return fail(SILT_ERR_INVALID, "null group");
+    for (int k = 0; k < n; ++k) {
+        for (silt_solver* s : g->strips)
+            if (int rc = silt_solver_step(s, 1)) return rc;
+        if (int rc = group_exchange(g)) return rc;
+    }
+    return SILT_OK;
+}
+
+// run_parallel rethrows the lowest rank's error (src/parallel.cpp:377-378)
+int silt_group_status(silt_group* g, silt_status* st) {
+    if (!g || !st) return fail(SILT_ERR_INVALID, "silt_group_status: null argument");
+    int first_rc = SILT_OK;
+    silt_status first{};
+    for (size_t k = 0; k < g->strips.size(); ++k) {
+        silt_status s{};
+        const int rc = silt_solver_status(g->strips[k], &s);
+        if (k == 0) first = s;
+        if (rc && !first_rc) {
+            first_rc = rc;
+            first = s;
+            if (rc == SILT_ERR_CUDA) break;
+        }
+    }
+    *st = first;
+    return first_rc;
+}
+
+int silt_group_resume(silt_group* g) {
+    if (!g) return fail(SILT_ERR_INVALID, "null group");
+    for (silt_solver* s : g->strips)
+        if (int rc = silt_solver_resume(s)) return rc;
+    return SILT_OK;
+}
+
+int silt_group_dt_log(silt_group* g, double* host_out, int64_t n) {
+    if (!g || g->strips.empty()) return fail(SILT_ERR_INVALID, "null group");
+    return silt_solver_dt_log(g->strips[0], host_out, n);
+}
+
+}  // extern "C"
+
+extern "C" {
+
 // run_serial on the GPU (src/parallel.cpp:208-259)
 int silt_run(const silt_problem* problem, const double* init_aos, const silt_run_plan* plan,
              int variant, double* out_aos, double* dt_log, int64_t dt_log_capacity,

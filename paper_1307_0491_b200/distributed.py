@@ -257,91 +257,56 @@ class StripRunner:
 
 class LocalStripGroup:
     """run_parallel(sc, 1, py) in ONE process (src/parallel.cpp:261-386): py
-    row strips, strip k on CUDA device ``devices[k % len(devices)]``, all
-    enqueued on per-device streams in lock step.  Ghost rows move with device
-    (or peer) copies and the axis-speed maxima are reduced on device, so the
-    per-step device protocol is exactly the one the NCCL driver runs.
+    row strips, strip k on CUDA device ``devices[k % len(devices)]`` — the
+    native strip group of the C ABI (silt_group_*): ghost rows move with
+    device/peer copies and the axis-speed maxima are reduced on device,
+    ordered by stream events, so no step needs a host round trip.
     """
 
     def __init__(self, problem, py: int, devices=(0,), variant: int = abi.VARIANT_FAST):
-        import torch
+        import ctypes as C
         from . import native
-        ny = 1 if problem.dim == 1 else problem.ny
-        if py < 1 or py > ny:
-            raise ValueError("partition: every worker needs at least one cell per axis")
-        if problem.dim == 1 and py != 1:
-            raise ValueError("partition: 1D grids require py == 1")
-        self.problem, self.py = problem, py
-        periodic_y = problem.dim == 2 and problem.bc[abi.SOUTH].type == abi.BC_PERIODIC
-        self.strips = []
-        for r in range(py):
-            j0, n = block_range(ny, py, r)
-            south, north = neighbours(r, py, periodic_y)
-            dev = devices[r % len(devices)]
-            st = abi.SiltStrip(j0, n, int(south is not None), int(north is not None))
-            s = native.Solver(problem, st, dev, variant)
-            stream = torch.cuda.Stream(device=dev)
-            s.set_stream(stream.cuda_stream)
-            ex = s.exchange_ptrs()
-            d = torch.device("cuda", dev)
-            wrap = (lambda ptr, n=ex.row_doubles, d=d:
-                    torch.as_tensor(_CAI(ptr, n), device=d) if ptr else None)
-            self.strips.append(dict(solver=s, stream=stream, device=d, j0=j0, n=n,
-                                    south=south, north=north,
-                                    send_s=wrap(ex.send_south), send_n=wrap(ex.send_north),
-                                    recv_s=wrap(ex.recv_south), recv_n=wrap(ex.recv_north)))
-
-    def _sync_streams(self):
-        for s in self.strips:
-            s["stream"].synchronize()
-
-    def _exchange(self):
-        import torch
-        if self.py == 1:
-            return
-        self._sync_streams()
-        with torch.no_grad():
-            for s in self.strips:
-                if s["south"] is not None:
-                    src = self.strips[s["south"]]
-                    s["recv_s"].copy_(src["send_n"])
-                if s["north"] is not None:
-                    src = self.strips[s["north"]]
-                    s["recv_n"].copy_(src["send_s"])
-            slots = [torch.as_tensor(_CAI(s["solver"].reduce_slot(), 2), device=s["device"])
-                     for s in self.strips]
-            m = slots[0].clone()
-            for t in slots[1:]:
-                m = torch.maximum(m, t.to(m.device))
-            for t in slots:
-                t.copy_(m.to(t.device))
-        torch.cuda.synchronize()
+        self.N = native
+        self.L = native.lib()
+        self.problem = problem
+        self.nx = problem.nx
+        self.ny = 1 if problem.dim == 1 else problem.ny
+        devs = (C.c_int * len(devices))(*devices)
+        self.h = C.c_void_p()
+        native.check(self.L.silt_group_create(C.byref(problem), int(py), devs, len(devices),
+                                              variant, C.byref(self.h)))
 
     def upload(self, field: np.ndarray):
-        for s in self.strips:
-            s["solver"].upload(np.ascontiguousarray(field[s["j0"]:s["j0"] + s["n"]]))
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        self.N.check(self.L.silt_group_upload(self.h, self.N._dp(f)))
 
     def begin(self, t_end: float = np.inf, max_steps: int = -1, snapshots=(), dt_cap: int = 0):
-        for s in self.strips:
-            s["solver"].begin(t_end=t_end, max_steps=max_steps, snapshots=snapshots, dt_cap=dt_cap)
-        self._exchange()
+        import ctypes as C
+        plan, keep = self.N._plan(t_end, max_steps, snapshots, dt_cap)
+        self.N.check(self.L.silt_group_begin(self.h, C.byref(plan)))
+        del keep
 
     def step(self, n: int = 1):
-        for _ in range(n):
-            for s in self.strips:
-                s["solver"].step(1)
-            self._exchange()
+        self.N.check(self.L.silt_group_step(self.h, int(n)))
 
     def status(self):
-        sts = [s["solver"].status() for s in self.strips]
-        return sts[0]
+        import ctypes as C
+        st = abi.SiltStatus()
+        self.N.check(self.L.silt_group_status(self.h, C.byref(st)))
+        return st
 
     def resume(self):
-        for s in self.strips:
-            s["solver"].resume()
+        self.N.check(self.L.silt_group_resume(self.h))
+
+    def dt_log(self, n: int) -> np.ndarray:
+        out = np.empty(n)
+        self.N.check(self.L.silt_group_dt_log(self.h, self.N._dp(out), int(n)))
+        return out
 
     def gather(self) -> np.ndarray:
-        return np.concatenate([s["solver"].download() for s in self.strips], axis=0)
+        out = np.empty((self.ny, self.nx, 4))
+        self.N.check(self.L.silt_group_download(self.h, self.N._dp(out)))
+        return out
 
     def run(self, batch: int = 8, on_snapshot=None):
         while True:
@@ -356,5 +321,6 @@ class LocalStripGroup:
                 return st
 
     def close(self):
-        for s in self.strips:
-            s["solver"].close()
+        if self.h:
+            self.L.silt_group_destroy(self.h)
+            self.h = None

@@ -81,6 +81,16 @@ def lib() -> C.CDLL:
         "silt_step_padded": ([_P, _D, C.c_double, C.c_int], C.c_int),
         "silt_riemann_batch": ([_P, _D, _D, C.c_int64, C.c_int, C.c_int, _D], C.c_int),
         "silt_selftest_math": ([_D, _D, C.c_int64, _D], C.c_int),
+        "silt_group_create": ([_P, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int,
+                               C.POINTER(_VP)], C.c_int),
+        "silt_group_destroy": ([_VP], C.c_int),
+        "silt_group_upload": ([_VP, _D], C.c_int),
+        "silt_group_download": ([_VP, _D], C.c_int),
+        "silt_group_begin": ([_VP, C.POINTER(SiltRunPlan)], C.c_int),
+        "silt_group_step": ([_VP, C.c_int], C.c_int),
+        "silt_group_status": ([_VP, C.POINTER(SiltStatus)], C.c_int),
+        "silt_group_resume": ([_VP], C.c_int),
+        "silt_group_dt_log": ([_VP, _D, C.c_int64], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
