@@ -343,39 +343,53 @@ __device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4],
 #define SILT_STEP_MIN_BLOCKS 3
 #endif
 
-// Source of one field of cell (col, row) for the cp.async row prefetch: the
-// interior plane, a ghost-row buffer, a caller-given ghost column, or the
-// interior cell a physical x-boundary ghost is derived from (fixed up after
-// the copy lands, see fix_xghost).
-__device__ __forceinline__ const double* cell_src(const StepArgs& A, int p, int col, int row,
-                                                  int f) {
+// Per-lane source of the cp.async row prefetch.  The column mapping (interior
+// column, periodic wrap, the interior cell a physical x-ghost is derived from,
+// or a caller-given ghost column) is fixed per lane, so it is resolved once:
+// interior rows then cost one multiply-add per field.  Rows -1 / ny come from
+// the ghost-row buffers (physical BC rows, or rows received from a neighbour).
+struct RowSrc {
+    const double* base[4];
+    size_t stride;  // row stride of base (pitch, or 1 for a given ghost column)
+    int col_clamped;
+};
+
+__device__ __forceinline__ RowSrc row_src(const StepArgs& A, int p, int col) {
+    RowSrc s;
     const int nx = A.nx;
-    if (row < 0 || row >= A.ny) {
-        const double* g;
-        if (row < 0)
-            g = A.south_nbr ? A.recv_s : A.ghost_s[p];
-        else
-            g = A.north_nbr ? A.recv_n : A.ghost_n[p];
-        return g + (size_t)f * nx + min(max(col, 0), nx - 1);
-    }
     int c;
+    s.stride = A.pitch;
     if (col == -1 || col == nx) {
         const int side = col < 0 ? SILT_WEST : SILT_EAST;
         const int t = A.bc_type[side];
-        if (t == SILT_BC_GIVEN)
-            return (side == SILT_WEST ? A.ghost_w : A.ghost_e) + (size_t)f * A.ny + row;
-        if (t == SILT_BC_PERIODIC)
-            c = col < 0 ? nx - 1 : 0;
-        else
-            c = col < 0 ? 0 : nx - 1;
+        if (t == SILT_BC_GIVEN) {
+            const double* g = side == SILT_WEST ? A.ghost_w : A.ghost_e;
+#pragma unroll
+            for (int f = 0; f < 4; ++f) s.base[f] = g + (size_t)f * A.ny;
+            s.stride = 1;
+            s.col_clamped = col < 0 ? 0 : nx - 1;
+            return s;
+        }
+        c = (t == SILT_BC_PERIODIC) ? (col < 0 ? nx - 1 : 0) : (col < 0 ? 0 : nx - 1);
     } else {
         c = min(max(col, 0), nx - 1);  // dead lanes: any valid cell
     }
-    return A.state[p][f] + (size_t)row * A.pitch + c;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) s.base[f] = A.state[p][f] + c;
+    s.col_clamped = min(max(col, 0), nx - 1);
+    return s;
+}
+
+__device__ __forceinline__ const double* row_field(const StepArgs& A, const RowSrc& s, int p,
+                                                   int row, int f) {
+    if (row >= 0 && row < A.ny) return s.base[f] + (size_t)row * s.stride;
+    const double* g = row < 0 ? (A.south_nbr ? A.recv_s : A.ghost_s[p])
+                              : (A.north_nbr ? A.recv_n : A.ghost_n[p]);
+    return g + (size_t)f * A.nx + s.col_clamped;
 }
 
 // Physical x-boundary ghost (apply_bc_side, src/scenarios.cpp:78-99) applied
-// to the interior cell copied by cell_src.
+// to the interior cell the row prefetch copied (row_src).
 __device__ __forceinline__ void fix_xghost(const StepArgs& A, int col, int row, double c[4]) {
     if (row < 0 || row >= A.ny || (col != -1 && col != A.nx)) return;
     const int side = col < 0 ? SILT_WEST : SILT_EAST;
@@ -391,7 +405,8 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-__device__ __forceinline__ void side_to_ring(double (*ring)[kStepThreads], const Side& s, int lane) {
+template <int W>
+__device__ __forceinline__ void side_to_ring(double (*ring)[W], const Side& s, int lane) {
     ring[0][lane] = s.h;
     ring[1][lane] = s.hun;
     ring[2][lane] = s.pi;
@@ -405,7 +420,8 @@ __device__ __forceinline__ void side_to_ring(double (*ring)[kStepThreads], const
     ring[10][lane] = __hiloint2double(0, s.wet | (s.moving << 1));
 }
 
-__device__ __forceinline__ Side side_from_ring(const double (*ring)[kStepThreads], int lane) {
+template <int W>
+__device__ __forceinline__ Side side_from_ring(const double (*ring)[W], int lane) {
     Side s;
     s.h = ring[0][lane];
     s.hun = ring[1][lane];
@@ -435,13 +451,26 @@ __device__ __forceinline__ Side side_of(const StepArgs& A, const double c[4], bo
 }
 
 template <bool S>
+__device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], Side& sx, Side& sy) {
+    if constexpr (S) {
+        sx = make_side_ref(A.P, c[0], c[1], c[2], c[3]);
+        sy = make_side_ref(A.P, c[0], c[2], c[1], c[3]);
+    } else {
+        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
+        sx = make_side_fast(A.P, pre, true);
+        sy = make_side_fast(A.P, pre, false);
+    }
+}
+
+template <bool S>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
     // Per-thread march state in shared memory (SoA by thread: conflict-free),
     // so that registers at each face solve hold little beyond the solver.
-    __shared__ double sh_side[11][kStepThreads];   // y-side terms of row r-1
-    __shared__ double sh_xs[4][kStepThreads];      // x-updated row r-1
-    __shared__ double sh_fy[4][kStepThreads];      // y face below row r-1: h, huR, hv, z
-    __shared__ double sh_row[2][4][kStepThreads];  // cp.async row prefetch
+    __shared__ double sh_side[11][kStepThreads];       // y-side terms of row r-1
+    __shared__ double sh_sx[11][kStepThreads + 1];     // x-side terms of row r (+1: lane 31 reads t+1)
+    __shared__ double sh_xs[4][kStepThreads];          // x-updated row r-1
+    __shared__ double sh_fy[4][kStepThreads];          // y face below row r-1: h, huR, hv, z
+    __shared__ double sh_row[2][4][kStepThreads];      // cp.async row prefetch
 
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
@@ -464,11 +493,11 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const double cx = d.dt / A.dx;
     const double cy = d.dt / A.dy;
     const double href = __longlong_as_double((long long)cur.hmax);
-    double(*side_prev)[kStepThreads] = sh_side;
+    const RowSrc src = row_src(A, p, col);
 
     Reduce R{0.0, 0.0, 0.0, 0u};
 #pragma unroll
-    for (int f = 0; f < 4; ++f) cp_async8(&sh_row[0][f][t], cell_src(A, p, col, jb - 1, f));
+    for (int f = 0; f < 4; ++f) cp_async8(&sh_row[0][f][t], row_field(A, src, p, jb - 1, f));
     cp_async_commit();
     int buf = 0;
 #pragma unroll 1
@@ -476,7 +505,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         if (r < je) {
 #pragma unroll
             for (int f = 0; f < 4; ++f)
-                cp_async8(&sh_row[buf ^ 1][f][t], cell_src(A, p, col, r + 1, f));
+                cp_async8(&sh_row[buf ^ 1][f][t], row_field(A, src, p, r + 1, f));
         }
         cp_async_commit();
         cp_async_wait1();
@@ -488,18 +517,20 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         const bool own_row = r >= jb && r < je;
 
         // y face between rows r-1 and r (normal = v, transverse = u), solved
-        // first so that only this row's x-side is carried across it
+        // first; the x-side waits in shared memory for the x face
         Flux fy{0, 0, 0, 0, 0};
         {
-            const Side sy = side_of<S>(A, c, false);
+            Side sx, sy;
+            sides_of<S>(A, c, sx, sy);
+            if (own_row) side_to_ring(sh_sx, sx, t);
             if (r > jb - 1 && owned) {
-                const Side lo = side_from_ring(side_prev, t);
+                const Side lo = side_from_ring(sh_side, t);
                 if (!face_flux<S>(A.P, lo, sy, fy)) {
                     const double info[6] = {lo.h, lo.un, lo.z, sy.h, sy.un, sy.z};
                     record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
                 }
             }
-            side_to_ring(side_prev, sy, t);
+            side_to_ring(sh_side, sy, t);
         }
         if (r - 1 >= jb && owned) {
             // y update of row r-1 (src/stepper.cpp:181-186) + check_depth
@@ -522,12 +553,13 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         sh_fy[1][t] = fy.huR;
         sh_fy[2][t] = fy.hv;
         sh_fy[3][t] = fy.z;
+        __syncwarp();
         // x faces: this lane solves the face between col and col+1
         Flux fx{0, 0, 0, 0, 0};
-        {
-            const Side sx = side_of<S>(A, c, true);
-            const Side right = shfl_down_side(sx);
-            if (xface && !face_flux<S>(A.P, sx, right, fx)) {
+        if (xface) {
+            const Side sx = side_from_ring(sh_sx, t);
+            const Side right = side_from_ring(sh_sx, t + 1);
+            if (!face_flux<S>(A.P, sx, right, fx)) {
                 const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
                 record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
             }
@@ -539,6 +571,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         sh_xs[1][t] = c[1] - cx * (fx.huL - lhuR);
         sh_xs[2][t] = c[2] - cx * (fx.hv - lhv);
         sh_xs[3][t] = c[3] - cx * (fx.z - lz);
+        __syncwarp();
     }
     reduce_flush(R, nxt);
 }

@@ -600,19 +600,41 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
     const double ustar = 0.5 * (m2 + m4 - b * c.kappa);
     const double wstar = l.omega + m2 * e.dzl;
     const double a2 = a * a;
-    double sp[5] = {c.lam, m2, ustar, m4, c.rho};
-    double ex[5] = {0, (a2 - b * b) * (e.t2 - e.t1), 0, (a2 - b * b) * (e.t4 - e.t3), 0};
-    const int rg = first_nonneg(sp);
+    // Sample at xi = 0: the region left of the first wave with non-negative
+    // speed among {lam, m2, ustar, m4, rho} (src/riemann.cpp:302-312).
     double hu, uu, p, w;
-    switch (rg) {
-        case 0: hu = l.hun; uu = l.un; p = l.pi; w = l.omega; break;
-        case 1: region_from_tau<S>(e.t1, c.lam + a * e.t1, kl - a2 * e.t1, l.omega, hu, uu, p, w); break;
-        case 2: region_from_tau<S>(e.t2, ustar, kl - a2 * e.t2, wstar, hu, uu, p, w); break;
-        case 3: region_from_tau<S>(e.t3, ustar, kr - a2 * e.t3, wstar, hu, uu, p, w); break;
-        case 4: region_from_tau<S>(e.t4, c.rho - a * e.t4, kr - a2 * e.t4, r.omega, hu, uu, p, w); break;
-        default: hu = r.hun; uu = r.un; p = r.pi; w = r.omega; break;
+    if (c.lam >= 0.0) {
+        hu = l.hun; uu = l.un; p = l.pi; w = l.omega;
+    } else if (m2 >= 0.0) {
+        region_from_tau<S>(e.t1, c.lam + a * e.t1, kl - a2 * e.t1, l.omega, hu, uu, p, w);
+    } else if (ustar >= 0.0) {
+        region_from_tau<S>(e.t2, ustar, kl - a2 * e.t2, wstar, hu, uu, p, w);
+    } else if (m4 >= 0.0) {
+        region_from_tau<S>(e.t3, ustar, kr - a2 * e.t3, wstar, hu, uu, p, w);
+    } else if (c.rho >= 0.0) {
+        region_from_tau<S>(e.t4, c.rho - a * e.t4, kr - a2 * e.t4, r.omega, hu, uu, p, w);
+    } else {
+        hu = r.hun; uu = r.un; p = r.pi; w = r.omega;
     }
-    publish(sp, ex, hu, uu, p, w, false, F);
+    // Momentum exchange split by wave sign (:313-324).  Only waves 1 and 3
+    // carry exchange in this ordering; the others add +0.0 to partial sums that
+    // are never -0.0, an identity, so the sums are bit-identical to the loop.
+    const double ex1 = (a2 - b * b) * (e.t2 - e.t1);
+    const double ex3 = (a2 - b * b) * (e.t4 - e.t3);
+    double mneg = 0.0, mpos = 0.0;
+    if (m2 < 0.0)
+        mneg += ex1;
+    else
+        mpos += ex1;
+    if (m4 < 0.0)
+        mneg += ex3;
+    else
+        mpos += ex3;
+    F.h = hu;
+    F.z = w;
+    const double base = hu * uu + p;
+    F.huL = base + mneg;
+    F.huR = base - mpos;
     return kSolved;
 }
 
@@ -625,9 +647,14 @@ __device__ __forceinline__ bool face_flux_general_impl(const Params& P, const Si
                                                        Flux& F) {
     F.h = F.huL = F.huR = F.hv = F.z = 0.0;
     if (!l.wet && !r.wet) return true;  // inert interface: a = b = 0
-    const double a0 = P.safety * smax(smax(0.0, l.a_side), r.a_side);
-    const double b0 =
-        (l.moving || r.moving) ? P.safety * dsqrt<S>(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
+    double a0, b0;
+    if constexpr (S) {
+        a0 = P.safety * smax(smax(0.0, l.a_side), r.a_side);
+        b0 = (l.moving || r.moving) ? P.safety * sqrt(smax(smax(0.0, l.b2_side), r.b2_side)) : 0.0;
+    } else {  // side terms are >= 0 (exactly 0 when dry)
+        a0 = P.safety * smax(l.a_side, r.a_side);
+        b0 = (l.moving || r.moving) ? P.safety * fsqrt(smax(l.b2_side, r.b2_side)) : 0.0;
+    }
     double a = a0, b = b0;
     bool ok = false;
     for (int attempt = 0; attempt <= kMaxEnlarge; ++attempt) {
