@@ -231,3 +231,59 @@ def test_strip_group_bitwise(N, golden, case, py):
             assert np.array_equal(out, data[f"{case}_final"])
         else:
             assert np.all(normwise(out, data[f"{case}_final"]) <= FIELD_TOL)
+
+
+def _device_run(N, p, init, steps, variant):
+    s = N.Solver(p, variant=variant)
+    s.upload(init)
+    s.begin(max_steps=steps, dt_cap=steps)
+    st = s.run(batch=64)
+    out = s.download()
+    log = s.dt_log(st.steps)
+    s.close()
+    return out, st, log
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties(N):
+    """C4 at its full 16384^2 size (BASELINE configs[3]), 40 steps, where the
+    oracle is too slow: (1) mirror symmetry about y = 500 m (the mound is
+    centred on it; hv odd, the rest even) to 5e-12 as in the reference's
+    y-symmetry test (tests/test_stepper.cpp:262-304); (2) water and bed volume
+    conserved (nothing has reached the boundary); (3) FAST == STRICT on the
+    full field within the parity bar, dt logs within 1e-12."""
+    p, init, _ = scenarios.dune_2d(16384)
+    steps = 40
+    fo, fst, flog = _device_run(N, p, init, steps, abi.VARIANT_FAST)
+    assert fst.steps == steps
+    mir = fo[::-1]
+    for f, sign in ((0, 1), (1, 1), (2, -1), (3, 1)):
+        scale = max(1.0, np.abs(fo[..., f]).max())
+        assert np.max(np.abs(fo[..., f] - sign * mir[..., f])) <= 5e-12 * scale, f
+    for f in (0, 3):
+        s0, s1 = init[..., f].sum(), fo[..., f].sum()
+        assert abs(s1 - s0) <= 1e-12 * abs(s0)
+    so, sst, slog = _device_run(N, p, init, steps, abi.VARIANT_STRICT)
+    assert sst.steps == steps
+    assert np.max(np.abs(flog - slog) / slog) <= DT_TOL
+    assert np.all(normwise(fo, so) <= FIELD_TOL)
+
+
+@pytest.mark.slow
+def test_c5_size_properties(N):
+    """C5 random bed at the per-GPU weak-scaling size (8192 x 4096 rows),
+    periodic in x and y so every cell is interior: water and bed volume are
+    conserved to round-off after 30 steps; FAST == STRICT within the bar."""
+    p, init, _ = scenarios.random_bed_2d(8192, 4096)
+    for s in range(4):
+        p.bc[s] = abi.bc("periodic")
+    steps = 30
+    fo, fst, flog = _device_run(N, p, init, steps, abi.VARIANT_FAST)
+    so, sst, slog = _device_run(N, p, init, steps, abi.VARIANT_STRICT)
+    assert fst.steps == sst.steps == steps
+    for f in (0, 3):
+        s0 = init[..., f].sum()
+        assert abs(fo[..., f].sum() - s0) <= 1e-12 * abs(s0)
+        assert abs(so[..., f].sum() - s0) <= 1e-12 * abs(s0)
+    assert np.max(np.abs(flog - slog) / slog) <= DT_TOL
+    assert np.all(normwise(fo, so) <= FIELD_TOL)
