@@ -687,8 +687,26 @@ __device__ __forceinline__ bool face_flux_general_impl(const Params& P, const Si
 // bounds_impl (src/relax_state.cpp:25-53) + the transverse flux of solve_face
 // (src/stepper.cpp:87).  Returns false when no positive fan exists after
 // kMaxEnlarge enlargements (the reference throws runtime_error).
+//
+// FAST only: identical wet states on both sides (bitwise) have an invisible
+// fan — every region is the input state, all exchange terms vanish — so the
+// flux is the physical flux of that state, returned exactly: F_h = hu_n,
+// F_z = omega, G- = G+ = hu_n u_n + pi (the reference's uniform-data KAT,
+// tests/test_riemann.cpp:195-212).  With contracted arithmetic the full solver
+// would leave an O(ulp) exchange residue G- != G+ that the reference's own
+// rounding happens to cancel, seeding noise into exactly uniform flow; the
+// exact form keeps quiescent regions exactly quiescent (and skips the solve).
 template <bool S>
 __device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const Side& r, Flux& F) {
+    if constexpr (!S) {
+        if (l.wet && l.h == r.h && l.hun == r.hun && l.ut == r.ut && l.z == r.z) {
+            F.h = l.hun;
+            F.z = l.omega;
+            F.huL = F.huR = fma(l.hun, l.un, l.pi);
+            F.hv = F.h != 0.0 ? F.h * l.ut : 0.0;
+            return true;
+        }
+    }
     return face_flux_general_impl<S>(P, l, r, F);
 }
 
