@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -253,6 +254,10 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     A.north_nbr = st.north_neighbor;
     A.per_y_self = problem->dim == 2 && problem->bc[SILT_SOUTH].type == SILT_BC_PERIODIC &&
                    !st.south_neighbor && !st.north_neighbor;
+    {
+        const char* q = std::getenv("SILT_QUIET_SKIP");
+        A.quiet_skip = (q && q[0] == '0') ? 0 : 1;
+    }
     A.dx = problem->dx;
     A.dy = problem->dim == 1 ? 1.0 : problem->dy;
     A.cfl = problem->cfl;

@@ -500,6 +500,22 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     for (int f = 0; f < 4; ++f) cp_async8(&sh_row[0][f][t], row_field(A, src, p, jb - 1, f));
     cp_async_commit();
     int buf = 0;
+    // Quiescent rows (FAST): when rows r-2, r-1 and r of this warp are bitwise
+    // equal and uniform across the warp (and wet), every face touching row r-1
+    // takes face_flux's exact uniform-state flux, so its update is exactly the
+    // identity and the shared-memory march state is already correct; the row
+    // is stored unchanged and its CFL speed comes from a one-entry cache.  The
+    // result is bit-identical to the full path (tests: SILT_QUIET_SKIP=0).
+    __shared__ long long sh_cprev[4][kStepThreads];   // previous row (bits)
+    // one-entry speed cache per warp (a skipped row is uniform across the warp)
+    __shared__ long long sh_qkey[4][kStepThreads / 32];
+    __shared__ double sh_qspd[2][kStepThreads / 32];
+    const int wid = t >> 5;
+    bool quiet_prev = false;
+    if constexpr (!S) {
+        if (A.quiet_skip && lane == 0) sh_qkey[0][wid] = -1;  // NaN payload: matches no state
+        __syncwarp();
+    }
 #pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
         if (r < je) {
@@ -515,6 +531,56 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         buf ^= 1;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
+
+        if constexpr (!S) {
+            if (A.quiet_skip) {
+                // vertical equality first (cheap); the horizontal test with
+                // shuffles only when the whole warp passed it
+                long long cb[4];
+                bool eqy = r > jb - 1;
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    cb[f] = __double_as_longlong(c[f]);
+                    eqy = eqy && cb[f] == sh_cprev[f][t];
+                    sh_cprev[f][t] = cb[f];
+                }
+                const bool wet = c[0] > A.P.h_dry;
+                bool quiet = __all_sync(0xffffffffu, !owned || (eqy && wet));
+                if (quiet) {
+                    bool eqx = true;
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) {  // every lane shuffles (no short-circuit)
+                        const long long rb = __shfl_down_sync(0xffffffffu, cb[f], 1);
+                        eqx = eqx && cb[f] == rb;
+                    }
+                    quiet = __all_sync(0xffffffffu, !xface || (eqx && wet));
+                }
+                const bool skip = quiet && quiet_prev && r - 1 >= jb;
+                quiet_prev = quiet;
+                if (skip) {
+                    if (owned) {  // row r-1 is unchanged: o == c
+                        const size_t off = (size_t)(r - 1) * A.pitch + col;
+#pragma unroll
+                        for (int f = 0; f < 4; ++f) A.state[q][f][off] = c[f];
+                        write_edges(A, q, col, r - 1, c);
+                        double qsx, qsy;
+                        if (cb[0] == sh_qkey[0][wid] && cb[1] == sh_qkey[1][wid] &&
+                            cb[2] == sh_qkey[2][wid] && cb[3] == sh_qkey[3][wid]) {
+                            qsx = sh_qspd[0][wid];
+                            qsy = sh_qspd[1][wid];
+                        } else {  // every writer stores the same values
+                            cell_speeds<S>(A, c, qsx, qsy);
+                            sh_qspd[0][wid] = qsx;
+                            sh_qspd[1][wid] = qsy;
+#pragma unroll
+                            for (int f = 0; f < 4; ++f) sh_qkey[f][wid] = cb[f];
+                        }
+                        reduce_fold(A, R, c, qsx, qsy);
+                    }
+                    continue;  // warp-uniform
+                }
+            }
+        }
 
         // y face between rows r-1 and r (normal = v, transverse = u), solved
         // first; the x-side waits in shared memory for the x face

@@ -58,6 +58,7 @@ struct StepArgs {
     int rows_per_block;
     int south_nbr, north_nbr, per_y_self;
     int write_edges_in_reduce;
+    int quiet_skip;         // FAST: skip provably unchanged quiescent rows
     double dx, dy, cfl;
     silt_dev::Params P;
     int bc_type[4];

@@ -164,14 +164,15 @@ __device__ __forceinline__ double normal_flux_derivative_ref(const Params& P, do
 // speed (FAST).  Same cut-offs as the reference (speed <= kUEps -> 0).
 __device__ __forceinline__ void grass_terms_fast(const Params& P, double un, double ut,
                                                  double s2, double& omega, double& dq) {
-    if (!(s2 > kUEps * kUEps)) {
-        omega = 0.0;
-        dq = 0.0;
+    const bool on = s2 > kUEps * kUEps;
+    if (P.m3) {  // q = a s^3: omega = a s^2 u_n, dq = a (3 u_n^2 + u_t^2); branch-free
+        omega = on ? P.a_g * s2 * un : 0.0;
+        dq = on ? P.a_g * fma(3.0 * un, un, ut * ut) : 0.0;
         return;
     }
-    if (P.m3) {  // q = a s^3: omega = a s^2 u_n, dq = a (3 u_n^2 + u_t^2)
-        omega = P.a_g * s2 * un;
-        dq = P.a_g * fma(3.0 * un, un, ut * ut);
+    if (!on) {
+        omega = 0.0;
+        dq = 0.0;
         return;
     }
     const double s = fsqrt(s2);
@@ -471,7 +472,7 @@ __device__ __forceinline__ Eval fo_eval(const FluidCtx& c, double m2, double m4)
     } else {
         e.id = rcp(e.d);
         e.dzl = (m4 * c.jz - c.jw) * e.id;
-        e.dzr = (m2 * c.jz - c.jw) * e.id;
+        e.dzr = 0.0;  // FAST: derived as dzl - jz where needed
         const double q12 = (e.t1 - e.t2) * (e.t1 + e.t2);
         const double q34 = (e.t3 - e.t4) * (e.t3 + e.t4);
         e.r1 = q12 + q34 + 2.0 * c.k * c.jz;
@@ -543,18 +544,28 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
     Eval e = fo_eval<S>(c, m2, m4);
     if (!e.valid) return kTry ? kBail : kIllPosed;
 
-    double tmax = tl;
-    tmax = (tmax < tr) ? tr : tmax;
-    tmax = (tmax < e.t1) ? e.t1 : tmax;
-    tmax = (tmax < e.t2) ? e.t2 : tmax;
-    tmax = (tmax < e.t3) ? e.t3 : tmax;
-    tmax = (tmax < e.t4) ? e.t4 : tmax;
-    const double res_scale = tmax * tmax + fabs(2.0 * c.k * c.jz) + fabs(2.0 * c.k * e.dzl) +
-                             fabs(2.0 * c.k * e.dzr);
-    const double tol = 1e-13 * res_scale + 1e-300;
+    // Stopping rule of the reference (src/riemann.cpp:201-204).  Every term of
+    // res_scale is >= 0 and tmax >= max(tl, tr), so res <= 1e-13 max(tl,tr)^2
+    // already implies res <= tol (rounding is monotone): the common
+    // converged-at-the-guess face skips the rest of the scale.  Same decision.
+    const double tlr = (tl < tr) ? tr : tl;
+    const bool early = res_norm(e) <= 1e-13 * (tlr * tlr);
+    double tol = 0.0;
+    if (!early) {
+        double tmax = tl;
+        tmax = (tmax < tr) ? tr : tmax;
+        tmax = (tmax < e.t1) ? e.t1 : tmax;
+        tmax = (tmax < e.t2) ? e.t2 : tmax;
+        tmax = (tmax < e.t3) ? e.t3 : tmax;
+        tmax = (tmax < e.t4) ? e.t4 : tmax;
+        const double dzr = S ? e.dzr : e.dzl - c.jz;  // FAST: dzl - dzr == jz
+        const double res_scale = tmax * tmax + fabs(2.0 * c.k * c.jz) +
+                                 fabs(2.0 * c.k * e.dzl) + fabs(2.0 * c.k * dzr);
+        tol = 1e-13 * res_scale + 1e-300;
+    }
 
     int it = 0;
-    while (res_norm(e) > tol) {
+    while (!early && res_norm(e) > tol) {
         if (++it > (kTry ? kTryNewton : kMaxNewton)) return kTry ? kBail : kIllPosed;
         double j11, j12, j21, j22, det, step2, step4;
         if constexpr (S) {

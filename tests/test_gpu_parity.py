@@ -291,3 +291,26 @@ def test_c5_size_properties(N):
         assert abs(so[..., f].sum() - s0) <= 1e-12 * abs(s0)
     assert np.max(np.abs(flog - slog) / slog) <= DT_TOL
     assert np.all(normwise(fo, so) <= FIELD_TOL)
+
+
+@pytest.mark.parametrize("case", ["C3", "C4s", "bc_inflow_wall"])
+def test_quiet_row_skip_is_bit_identical(N, golden, case, monkeypatch):
+    """The quiescent-row skip of the FAST step kernel changes no bit: runs with
+    SILT_QUIET_SKIP=0 (full path everywhere) and =1 agree exactly."""
+    if case == "C3":
+        p, init, _ = scenarios.dune_2d(1024)
+        steps = 300
+    elif case == "C4s":
+        p, init, _ = scenarios.dune_2d(4096)
+        steps = 60
+    else:
+        data, meta = golden
+        m = meta["cases"][case]
+        p, init, steps = problem_from_meta(m), data[f"{case}_init"], m["max_steps"]
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SILT_QUIET_SKIP", flag)
+        outs.append(N.run(p, init, max_steps=steps, variant=abi.VARIANT_FAST))
+    assert outs[0][2] == outs[1][2] == steps
+    assert np.array_equal(outs[0][3], outs[1][3])
+    assert np.array_equal(outs[0][0], outs[1][0])
