@@ -231,6 +231,8 @@ def main():
     ap.add_argument("--variant", default="fast", choices=["fast", "strict"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"],
+                    help="row strips for N > 1: equal estimated work (default) or block_range")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -238,14 +240,23 @@ def main():
 
     import torch
     from paper_1307_0491_b200 import abi, native
-    from paper_1307_0491_b200.distributed import StripRunner, init_dist
+    from paper_1307_0491_b200.distributed import (StripRunner, balanced_partition, init_dist,
+                                                  row_costs)
 
     world, rank, local = init_dist(args.gpus)
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     variant = abi.VARIANT_FAST if args.variant == "fast" else abi.VARIANT_STRICT
     p = build_global_problem(args.workload, world)
-    runner = StripRunner(p, world, rank, device=local, variant=variant)
+    partition = None
+    if world > 1 and args.partition == "balanced" and WORKLOADS[args.workload]["kind"] == "dune":
+        # work-balanced row strips (quiescent rows are cheaper); every rank
+        # derives the same cut from the same initial field
+        full = device_initial_rows(args.workload, p, 0, p.ny, device)
+        partition = balanced_partition(row_costs(full), world)
+        del full
+        torch.cuda.empty_cache()
+    runner = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
     j0, nrows = runner.j0, runner.nrows
     init = device_initial_rows(args.workload, p, j0, nrows, device)
     runner.upload_device(init)
@@ -296,7 +307,7 @@ def main():
         host = torch.empty((nrows, p.nx, 4), dtype=torch.float64, pin_memory=True)
         host.copy_(device_initial_rows(args.workload, p, j0, nrows, device).cpu())
         out = torch.empty_like(host, pin_memory=True)
-        runner2 = StripRunner(p, world, rank, device=local, variant=variant)
+        runner2 = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
         runner2.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -343,6 +354,7 @@ def main():
             "config": {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
                        "nx": p.nx, "ny": p.ny, "rows_per_gpu": nrows,
                        "parallelism": f"row strips x{world}",
+                       "partition": (args.partition if world > 1 else "single strip"),
                        "l2": "state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -45,6 +45,77 @@ def neighbours(rank: int, world: int, periodic_y: bool):
     return south, north
 
 
+def balanced_partition(row_cost, parts: int):
+    """Row strips of (approximately) equal total cost: returns [(offset,
+    count)] with every count >= 1.  Any partition gives bit-identical results
+    (the reference's layout contract, tests/test_parallel.cpp:215-238), so the
+    strips may follow the work instead of block_range's equal row counts."""
+    cost = np.asarray(row_cost, dtype=np.float64)
+    n = cost.size
+    if parts < 1 or parts > n:
+        raise ValueError("partition: every worker needs at least one cell per axis")
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    cuts = [0]
+    for k in range(1, parts):
+        target = cum[-1] * k / parts
+        c = int(np.searchsorted(cum, target))
+        c = max(c, cuts[-1] + 1)            # >= 1 row per strip
+        c = min(c, n - (parts - k))         # leave >= 1 row for each later strip
+        cuts.append(c)
+    cuts.append(n)
+    return [(cuts[k], cuts[k + 1] - cuts[k]) for k in range(parts)]
+
+
+QUIET_COST = 1.0 / 5.5  # measured: a quiescent 30-cell warp segment vs an active one
+
+
+def row_costs(field, h_dry: float = 1e-8, seg: int = 30, halo: int = 32):
+    """Estimated step cost per row of a (ny, nx, 4) field (numpy or torch):
+    30-cell segments whose cells equal their x and y neighbours are quiescent
+    (the step kernel skips them), the rest pay the full Riemann solves.  The
+    active set is dilated by ``halo`` rows to cover waves spreading during the
+    run."""
+    try:
+        import torch
+        is_t = isinstance(field, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_t = False
+    if is_t:
+        f = field
+        same_x = (f[:, 1:] == f[:, :-1]).all(dim=-1)
+        same_y = (f[1:] == f[:-1]).all(dim=-1)
+        q = torch.ones(f.shape[:2], dtype=torch.bool, device=f.device)
+        q[:, 1:] &= same_x
+        q[:, :-1] &= same_x
+        q[1:] &= same_y
+        q[:-1] &= same_y
+        q &= f[..., 0] > h_dry
+        q = q.cpu().numpy()
+    else:
+        f = np.asarray(field)
+        same_x = (f[:, 1:] == f[:, :-1]).all(axis=-1)
+        same_y = (f[1:] == f[:-1]).all(axis=-1)
+        q = np.ones(f.shape[:2], dtype=bool)
+        q[:, 1:] &= same_x
+        q[:, :-1] &= same_x
+        q[1:] &= same_y
+        q[:-1] &= same_y
+        q &= f[..., 0] > h_dry
+    ny, nx = q.shape
+    nseg = (nx + seg - 1) // seg
+    pad = np.ones((ny, nseg * seg), dtype=bool)
+    pad[:, :nx] = q
+    seg_quiet = pad.reshape(ny, nseg, seg).all(axis=2)
+    active = ~seg_quiet
+    if halo > 0:  # dilate along y
+        act = active.copy()
+        for d in range(1, halo + 1):
+            act[d:] |= active[:-d]
+            act[:-d] |= active[d:]
+        active = act
+    return active.sum(axis=1) + QUIET_COST * (~active).sum(axis=1)
+
+
 def init_dist(gpus: int = 1, backend: str | None = None):
     """(world, rank, local_rank); initialises torch.distributed when world > 1."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -79,7 +150,7 @@ class StripRunner:
     """
 
     def __init__(self, problem, world: int, rank: int, device: int = 0,
-                 variant: int = abi.VARIANT_FAST, solver_factory=None):
+                 variant: int = abi.VARIANT_FAST, solver_factory=None, partition=None):
         self.problem = problem
         self.world, self.rank = world, rank
         ny = 1 if problem.dim == 1 else problem.ny
@@ -87,7 +158,12 @@ class StripRunner:
             raise ValueError("partition: every worker needs at least one cell per axis")
         if problem.dim == 1 and world > 1:
             raise ValueError("partition: 1D grids require py == 1")
-        self.j0, self.nrows = block_range(ny, world, rank)
+        if partition is None:  # block_range, the reference's partition
+            self.j0, self.nrows = block_range(ny, world, rank)
+        else:  # e.g. balanced_partition(row_costs(...), world): [(j0, n)] per rank
+            if len(partition) != world or sum(n for _, n in partition) != ny:
+                raise ValueError("partition: strips must cover the grid once")
+            self.j0, self.nrows = partition[rank]
         periodic_y = problem.dim == 2 and problem.bc[abi.SOUTH].type == abi.BC_PERIODIC
         self.south, self.north = neighbours(rank, world, periodic_y)
         strip = abi.SiltStrip(self.j0, self.nrows, int(self.south is not None),

@@ -47,7 +47,7 @@ def test_neighbours():
     assert neighbours(1, 2, True) == (0, 0)
 
 
-def _worker(rank, world, port, case, out_dir):
+def _worker(rank, world, port, case, out_dir, partition=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     sys.path.insert(0, ROOT)
@@ -65,7 +65,7 @@ def _worker(rank, world, port, case, out_dir):
     def factory(problem, strip):
         return StripOracle(problem, strip, orc, init[strip.j0:strip.j0 + strip.ny_local])
 
-    runner = StripRunner(p, world, rank, solver_factory=factory)
+    runner = StripRunner(p, world, rank, solver_factory=factory, partition=partition)
     runner.begin(max_steps=steps, snapshots=snaps)
     seen = []
     st = runner.run(batch=3, on_snapshot=lambda t, f: seen.append(t))
@@ -103,3 +103,31 @@ def test_strips_bitwise_equal_serial(tmp_path, restatement, world, case):
     assert meta[1] == n and meta[0] == t
     assert list(meta[2:]) == [s for s in snaps if s <= t]
     assert np.array_equal(field, ref)
+
+
+def test_uneven_partition_bitwise_equal_serial(tmp_path, restatement):
+    """Work-balanced (uneven) strips: any partition gives the serial result."""
+    from paper_1307_0491_b200.distributed import balanced_partition, row_costs
+    p, init, _ = scenarios.dune_2d(32, a_g=0.5)
+    steps = 12
+    part = balanced_partition(row_costs(init, halo=2), 3)
+    assert len({n for _, n in part}) > 1  # genuinely uneven
+    ref, t, n, _ = restatement.run(p, init, max_steps=steps)
+    bcs = [p.bc[s] for s in range(4)]
+    mp.spawn(_worker, args=(3, _free_port(), (p, init, steps, (), bcs), str(tmp_path), part),
+             nprocs=3, join=True)
+    assert np.array_equal(np.load(tmp_path / "field.npy"), ref)
+
+
+def test_balanced_partition_properties():
+    from paper_1307_0491_b200.distributed import balanced_partition
+    rng = np.random.default_rng(3)
+    for n, parts in ((100, 7), (16384, 8), (9, 9)):
+        cost = rng.uniform(0.1, 5.0, n)
+        part = balanced_partition(cost, parts)
+        assert part[0][0] == 0 and sum(c for _, c in part) == n
+        assert all(c >= 1 for _, c in part)
+        assert all(part[k][0] + part[k][1] == part[k + 1][0] for k in range(parts - 1))
+        if n > 1000:
+            loads = [cost[o:o + c].sum() for o, c in part]
+            assert max(loads) <= 1.01 * sum(loads) / parts
