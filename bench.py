@@ -241,7 +241,7 @@ def main():
     import torch
     from paper_1307_0491_b200 import abi, native
     from paper_1307_0491_b200.distributed import (StripRunner, balanced_partition, init_dist,
-                                                  row_costs)
+                                                  refine_partition, row_costs)
 
     world, rank, local = init_dist(args.gpus)
     device = torch.device("cuda", local)
@@ -250,11 +250,29 @@ def main():
     p = build_global_problem(args.workload, world)
     partition = None
     if world > 1 and args.partition == "balanced" and WORKLOADS[args.workload]["kind"] == "dune":
-        # work-balanced row strips (quiescent rows are cheaper); every rank
-        # derives the same cut from the same initial field
+        # Work-balanced row strips (quiescent rows are cheaper).  Every rank
+        # derives the same cut from the same initial field; a short untimed
+        # pilot then rescales the model by each strip's measured step time.
         full = device_initial_rows(args.workload, p, 0, p.ny, device)
-        partition = balanced_partition(row_costs(full), world)
+        costs = row_costs(full)
         del full
+        torch.cuda.empty_cache()
+        partition = balanced_partition(costs, world)
+        pilot = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
+        pilot.upload_device(device_initial_rows(args.workload, p, pilot.j0, pilot.nrows, device))
+        pilot.begin(max_steps=8)
+        pilot.step(3)
+        pilot.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pilot.torch_stream)
+        pilot.solver.step(4)  # this strip alone (its step kernels)
+        e1.record(pilot.torch_stream)
+        torch.cuda.synchronize()
+        mine = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        times = [torch.zeros_like(mine) for _ in range(world)]
+        torch.distributed.all_gather(times, mine)
+        pilot.close()
+        partition = refine_partition(costs, partition, [float(x.item()) for x in times])
         torch.cuda.empty_cache()
     runner = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
     j0, nrows = runner.j0, runner.nrows

@@ -66,7 +66,7 @@ def balanced_partition(row_cost, parts: int):
     return [(cuts[k], cuts[k + 1] - cuts[k]) for k in range(parts)]
 
 
-QUIET_COST = 1.0 / 5.5  # measured: a quiescent 30-cell warp segment vs an active one
+QUIET_COST = 1.0 / 7.3  # measured on C4 strips (tools/strip_times.py): quiescent vs active segment
 
 
 def row_costs(field, h_dry: float = 1e-8, seg: int = 30, halo: int = 32):
@@ -114,6 +114,18 @@ def row_costs(field, h_dry: float = 1e-8, seg: int = 30, halo: int = 32):
             act[:-d] |= active[d:]
         active = act
     return active.sum(axis=1) + QUIET_COST * (~active).sum(axis=1)
+
+
+def refine_partition(row_cost, partition, strip_ms):
+    """One measured refinement: rescale the modelled cost of every row by its
+    strip's measured/predicted time, then re-cut.  strip_ms[k] is the measured
+    step time of partition[k]."""
+    cost = np.asarray(row_cost, dtype=np.float64).copy()
+    for (j0, n), t in zip(partition, strip_ms):
+        pred = cost[j0:j0 + n].sum()
+        if pred > 0 and t > 0:
+            cost[j0:j0 + n] *= t / pred
+    return balanced_partition(cost, len(partition))
 
 
 def init_dist(gpus: int = 1, backend: str | None = None):

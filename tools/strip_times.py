@@ -23,7 +23,8 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_1307_0491_b200 import abi, native  # noqa: E402
-from paper_1307_0491_b200.distributed import balanced_partition, block_range, row_costs  # noqa: E402
+from paper_1307_0491_b200.distributed import (balanced_partition, block_range,  # noqa: E402
+                                              refine_partition, row_costs)
 
 
 def strip_ms(p, full, j0, n, steps, warmup):
@@ -62,8 +63,11 @@ def main():
     t1 = strip_ms(p, full, 0, p.ny, a.steps, a.warmup)
     out = {"workload": a.workload, "t1_ms": t1, "runs": []}
     for n in (2, 4, 8):
+        bal = balanced_partition(costs, n)
+        bal_t = [strip_ms(p, full, j0, c, 4, 3) for j0, c in bal]  # the pilot
         for name, part in (("uniform", [block_range(p.ny, n, r) for r in range(n)]),
-                           ("balanced", balanced_partition(costs, n))):
+                           ("balanced", bal),
+                           ("refined", refine_partition(costs, bal, bal_t))):
             ts = [strip_ms(p, full, j0, c, a.steps, a.warmup) for j0, c in part]
             eff = t1 / (n * max(ts))
             out["runs"].append({"n": n, "partition": name, "rows": [c for _, c in part],
