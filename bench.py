@@ -49,6 +49,7 @@ WORKLOADS = {
     "C4": dict(kind="dune", n=16384, a_g=0.001, cfl=0.5),
     "C4s": dict(kind="dune", n=4096, a_g=0.001, cfl=0.5),  # profiling size
     "C5": dict(kind="random", nx=8192, ny_per_gpu=4096, a_g=0.01, cfl=0.4),
+    "Q": dict(kind="uniform", n=16384, a_g=0.001, cfl=0.5),  # diagnostics: quiescent-row path
 }
 
 
@@ -101,7 +102,7 @@ class ClockSampler:
 def build_global_problem(wl: str, world: int):
     from paper_1307_0491_b200 import abi
     w = WORKLOADS[wl]
-    if w["kind"] == "dune":
+    if w["kind"] in ("dune", "uniform"):
         n = w["n"]
         p = abi.make_problem(2, n, n, 1000.0 / n, 1000.0 / n, a_g=w["a_g"], cfl=w["cfl"])
     else:
@@ -119,7 +120,11 @@ def device_initial_rows(wl: str, p, j0: int, nrows: int, device):
     w = WORKLOADS[wl]
     nx = p.nx
     out = torch.zeros((nrows, nx, 4), dtype=torch.float64, device=device)
-    if w["kind"] == "dune":
+    if w["kind"] == "uniform":
+        out[..., 0] = 9.9
+        out[..., 1] = 10.0
+        out[..., 3] = 0.1
+    elif w["kind"] == "dune":
         wx = torch.from_numpy(S._sine_bump(S._centres(nx, p.dx), 300.0, 200.0)).to(device)
         wy_all = S._sine_bump(S._centres(p.ny, p.dy), 400.0, 200.0)
         wy = torch.from_numpy(np.ascontiguousarray(wy_all[j0:j0 + nrows])).to(device)

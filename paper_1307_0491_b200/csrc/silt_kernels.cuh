@@ -388,6 +388,26 @@ __device__ __forceinline__ const double* row_field(const StepArgs& A, const RowS
     return g + (size_t)f * A.nx + s.col_clamped;
 }
 
+__device__ __forceinline__ void cp_async8_s(unsigned dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+}
+
+// Prefetch the 4 fields of one row: a single range check and one 64-bit
+// offset per row; dst = shared address of field 0's slot, fields kStepThreads
+// doubles apart.
+__device__ __forceinline__ void prefetch_row(const StepArgs& A, const RowSrc& s, int p, int row,
+                                             unsigned dst) {
+    constexpr unsigned kFieldBytes = kStepThreads * sizeof(double);
+    if (row >= 0 && row < A.ny) {
+        const size_t off = (size_t)row * s.stride;
+#pragma unroll
+        for (int f = 0; f < 4; ++f) cp_async8_s(dst + f * kFieldBytes, s.base[f] + off);
+    } else {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) cp_async8_s(dst + f * kFieldBytes, row_field(A, s, p, row, f));
+    }
+}
+
 // Physical x-boundary ghost (apply_bc_side, src/scenarios.cpp:78-99) applied
 // to the interior cell the row prefetch copied (row_src).
 __device__ __forceinline__ void fix_xghost(const StepArgs& A, int col, int row, double c[4]) {
@@ -496,8 +516,13 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const RowSrc src = row_src(A, p, col);
 
     Reduce R{0.0, 0.0, 0.0, 0u};
-#pragma unroll
-    for (int f = 0; f < 4; ++f) cp_async8(&sh_row[0][f][t], row_field(A, src, p, jb - 1, f));
+    const unsigned row_sa0 = (unsigned)__cvta_generic_to_shared(&sh_row[0][0][t]);
+    const unsigned row_sa1 = (unsigned)__cvta_generic_to_shared(&sh_row[1][0][t]);
+    double* const out0 = A.state[q][0] + col;  // output cell (row 0) of each field
+    double* const out1 = A.state[q][1] + col;
+    double* const out2 = A.state[q][2] + col;
+    double* const out3 = A.state[q][3] + col;
+    prefetch_row(A, src, p, jb - 1, row_sa0);
     cp_async_commit();
     int buf = 0;
     // Quiescent rows (FAST): when rows r-2, r-1 and r of this warp are bitwise
@@ -507,22 +532,13 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     // is stored unchanged and its CFL speed comes from a one-entry cache.  The
     // result is bit-identical to the full path (tests: SILT_QUIET_SKIP=0).
     __shared__ long long sh_cprev[4][kStepThreads];   // previous row (bits)
-    // one-entry speed cache per warp (a skipped row is uniform across the warp)
-    __shared__ long long sh_qkey[4][kStepThreads / 32];
-    __shared__ double sh_qspd[2][kStepThreads / 32];
-    const int wid = t >> 5;
-    bool quiet_prev = false;
-    if constexpr (!S) {
-        if (A.quiet_skip && lane == 0) sh_qkey[0][wid] = -1;  // NaN payload: matches no state
-        __syncwarp();
-    }
+    // Speeds of the current quiescent streak (the state is the same on every
+    // skipped row of a streak), folded into the reduction once per streak.
+    bool quiet_prev = false, qvalid = false;
+    double qsx = 0.0, qsy = 0.0;
 #pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
-        if (r < je) {
-#pragma unroll
-            for (int f = 0; f < 4; ++f)
-                cp_async8(&sh_row[buf ^ 1][f][t], row_field(A, src, p, r + 1, f));
-        }
+        if (r < je) prefetch_row(A, src, p, r + 1, buf ? row_sa0 : row_sa1);
         cp_async_commit();
         cp_async_wait1();
         double c[4];
@@ -537,45 +553,39 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                 // vertical equality first (cheap); the horizontal test with
                 // shuffles only when the whole warp passed it
                 long long cb[4];
-                bool eqy = r > jb - 1;
+                unsigned long long dif = 0;
 #pragma unroll
                 for (int f = 0; f < 4; ++f) {
                     cb[f] = __double_as_longlong(c[f]);
-                    eqy = eqy && cb[f] == sh_cprev[f][t];
+                    dif |= (unsigned long long)(cb[f] ^ sh_cprev[f][t]);
                     sh_cprev[f][t] = cb[f];
                 }
+                const bool eqy = r > jb - 1 && dif == 0ull;
                 const bool wet = c[0] > A.P.h_dry;
                 bool quiet = __all_sync(0xffffffffu, !owned || (eqy && wet));
                 if (quiet) {
-                    bool eqx = true;
+                    unsigned long long difx = 0;
 #pragma unroll
-                    for (int f = 0; f < 4; ++f) {  // every lane shuffles (no short-circuit)
-                        const long long rb = __shfl_down_sync(0xffffffffu, cb[f], 1);
-                        eqx = eqx && cb[f] == rb;
-                    }
-                    quiet = __all_sync(0xffffffffu, !xface || (eqx && wet));
+                    for (int f = 0; f < 4; ++f)  // every lane shuffles
+                        difx |= (unsigned long long)(cb[f] ^ __shfl_down_sync(0xffffffffu, cb[f], 1));
+                    quiet = __all_sync(0xffffffffu, !xface || (difx == 0ull && wet));
                 }
                 const bool skip = quiet && quiet_prev && r - 1 >= jb;
                 quiet_prev = quiet;
+                if (!skip) qvalid = false;
                 if (skip) {
                     if (owned) {  // row r-1 is unchanged: o == c
-                        const size_t off = (size_t)(r - 1) * A.pitch + col;
-#pragma unroll
-                        for (int f = 0; f < 4; ++f) A.state[q][f][off] = c[f];
-                        write_edges(A, q, col, r - 1, c);
-                        double qsx, qsy;
-                        if (cb[0] == sh_qkey[0][wid] && cb[1] == sh_qkey[1][wid] &&
-                            cb[2] == sh_qkey[2][wid] && cb[3] == sh_qkey[3][wid]) {
-                            qsx = sh_qspd[0][wid];
-                            qsy = sh_qspd[1][wid];
-                        } else {  // every writer stores the same values
+                        const size_t off = (size_t)(r - 1) * A.pitch;
+                        out0[off] = c[0];
+                        out1[off] = c[1];
+                        out2[off] = c[2];
+                        out3[off] = c[3];
+                        if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, c);
+                        if (!qvalid) {  // first row of the streak: its speeds, folded once
                             cell_speeds<S>(A, c, qsx, qsy);
-                            sh_qspd[0][wid] = qsx;
-                            sh_qspd[1][wid] = qsy;
-#pragma unroll
-                            for (int f = 0; f < 4; ++f) sh_qkey[f][wid] = cb[f];
+                            reduce_fold(A, R, c, qsx, qsy);
+                            qvalid = true;
                         }
-                        reduce_fold(A, R, c, qsx, qsy);
                     }
                     continue;  // warp-uniform
                 }
@@ -606,10 +616,12 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             o[1] = sh_xs[1][t] - cy * (fy.hv - sh_fy[2][t]);
             o[3] = sh_xs[3][t] - cy * (fy.z - sh_fy[3][t]);
             if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
-            const size_t off = (size_t)(r - 1) * A.pitch + col;
-#pragma unroll
-            for (int f = 0; f < 4; ++f) A.state[q][f][off] = o[f];
-            write_edges(A, q, col, r - 1, o);
+            const size_t off = (size_t)(r - 1) * A.pitch;
+            out0[off] = o[0];
+            out1[off] = o[1];
+            out2[off] = o[2];
+            out3[off] = o[3];
+            if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, o);
             double ssx, ssy;
             cell_speeds<S>(A, o, ssx, ssy);
             reduce_fold(A, R, o, ssx, ssy);
