@@ -424,6 +424,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;\n" ::); }
 
 template <int W>
 __device__ __forceinline__ void side_to_ring(double (*ring)[W], const Side& s, int lane) {
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     __shared__ double sh_sx[11][kStepThreads + 1];     // x-side terms of row r (+1: lane 31 reads t+1)
     __shared__ double sh_xs[4][kStepThreads];          // x-updated row r-1
     __shared__ double sh_fy[4][kStepThreads];          // y face below row r-1: h, huR, hv, z
-    __shared__ double sh_row[2][4][kStepThreads];      // cp.async row prefetch
+    __shared__ double sh_row[3][4][kStepThreads];      // cp.async ring, 2 rows ahead
 
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
@@ -517,14 +518,16 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
 
     Reduce R{0.0, 0.0, 0.0, 0u};
     const unsigned row_sa0 = (unsigned)__cvta_generic_to_shared(&sh_row[0][0][t]);
-    const unsigned row_sa1 = (unsigned)__cvta_generic_to_shared(&sh_row[1][0][t]);
+    constexpr unsigned kSlotBytes = 4 * kStepThreads * sizeof(double);
     double* const out0 = A.state[q][0] + col;  // output cell (row 0) of each field
     double* const out1 = A.state[q][1] + col;
     double* const out2 = A.state[q][2] + col;
     double* const out3 = A.state[q][3] + col;
     prefetch_row(A, src, p, jb - 1, row_sa0);
     cp_async_commit();
-    int buf = 0;
+    if (jb <= je) prefetch_row(A, src, p, jb, row_sa0 + kSlotBytes);
+    cp_async_commit();
+    int buf = 0;  // ring slot of row r
     // Quiescent rows (FAST): when rows r-2, r-1 and r of this warp are bitwise
     // equal and uniform across the warp (and wet), every face touching row r-1
     // takes face_flux's exact uniform-state flux, so its update is exactly the
@@ -538,13 +541,14 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     double qsx = 0.0, qsy = 0.0;
 #pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
-        if (r < je) prefetch_row(A, src, p, r + 1, buf ? row_sa0 : row_sa1);
+        const int ahead = buf == 0 ? 2 : buf - 1;  // slot of row r+2
+        if (r + 2 <= je) prefetch_row(A, src, p, r + 2, row_sa0 + ahead * kSlotBytes);
         cp_async_commit();
-        cp_async_wait1();
+        cp_async_wait2();  // row r landed; rows r+1, r+2 may be in flight
         double c[4];
 #pragma unroll
         for (int f = 0; f < 4; ++f) c[f] = sh_row[buf][f][t];
-        buf ^= 1;
+        buf = buf == 2 ? 0 : buf + 1;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
 
