@@ -174,6 +174,7 @@ int error_from(const Control& c, unsigned bits) {
     }
     if (bits & silt_dev::kErrNegDepth) return fail(SILT_ERR_RUNTIME, kNegDepthMsg);
     if (bits & silt_dev::kErrDry) return fail(SILT_ERR_INVALID, "cfl_dt: field is entirely dry");
+
     return fail(SILT_ERR_RUNTIME, "step: device error");
 }
 

@@ -389,7 +389,7 @@ __device__ __forceinline__ const double* row_field(const StepArgs& A, const RowS
 }
 
 __device__ __forceinline__ void cp_async8_s(unsigned dst, const double* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
 }
 
 // Prefetch the 4 fields of one row: a single range check and one 64-bit
@@ -420,11 +420,25 @@ __device__ __forceinline__ void fix_xghost(const StepArgs& A, int col, int row, 
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-__device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;\n" ::); }
+// "memory" clobbers: shared-memory reads of a slot must not move across the
+// wait that makes it valid, nor across the copy that overwrites it.
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait2() {
+    asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+}
+#ifndef SILT_RING
+#define SILT_RING 6
+#endif
+__device__ __forceinline__ void cp_async_wait_ring() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SILT_RING - 1) : "memory");
+}
 
 template <int W>
 __device__ __forceinline__ void side_to_ring(double (*ring)[W], const Side& s, int lane) {
@@ -483,15 +497,29 @@ __device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], S
     }
 }
 
+// SILT_RING: cp.async ring slots; rows are issued SILT_RING-1 ahead
+// Per-CTA shared memory of the 2D step (dynamic: above the 48 KB static cap).
+struct StepSmem {
+    double side[11][kStepThreads];        // y-side terms of row r-1
+    double sx[11][kStepThreads + 1];      // x-side terms of row r (+1: lane 31 reads t+1)
+    double xs[4][kStepThreads];           // x-updated row r-1
+    double fy[4][kStepThreads];           // y face below row r-1: h, huR, hv, z
+    double row[SILT_RING][4][kStepThreads];  // cp.async ring
+    long long cprev[4][kStepThreads];     // previous row (bits), quiescence test
+};
+
 template <bool S>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
     // Per-thread march state in shared memory (SoA by thread: conflict-free),
     // so that registers at each face solve hold little beyond the solver.
-    __shared__ double sh_side[11][kStepThreads];       // y-side terms of row r-1
-    __shared__ double sh_sx[11][kStepThreads + 1];     // x-side terms of row r (+1: lane 31 reads t+1)
-    __shared__ double sh_xs[4][kStepThreads];          // x-updated row r-1
-    __shared__ double sh_fy[4][kStepThreads];          // y face below row r-1: h, huR, hv, z
-    __shared__ double sh_row[3][4][kStepThreads];      // cp.async ring, 2 rows ahead
+    extern __shared__ __align__(16) unsigned char step_smem_raw[];
+    StepSmem& sm = *reinterpret_cast<StepSmem*>(step_smem_raw);
+    auto& sh_side = sm.side;
+    auto& sh_sx = sm.sx;
+    auto& sh_xs = sm.xs;
+    auto& sh_fy = sm.fy;
+    auto& sh_row = sm.row;
+    auto& sh_cprev = sm.cprev;
 
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
@@ -523,10 +551,11 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     double* const out1 = A.state[q][1] + col;
     double* const out2 = A.state[q][2] + col;
     double* const out3 = A.state[q][3] + col;
-    prefetch_row(A, src, p, jb - 1, row_sa0);
-    cp_async_commit();
-    if (jb <= je) prefetch_row(A, src, p, jb, row_sa0 + kSlotBytes);
-    cp_async_commit();
+#pragma unroll
+    for (int k = 0; k < SILT_RING - 1; ++k) {
+        if (jb - 1 + k <= je) prefetch_row(A, src, p, jb - 1 + k, row_sa0 + k * kSlotBytes);
+        cp_async_commit();
+    }
     int buf = 0;  // ring slot of row r
     // Quiescent rows (FAST): when rows r-2, r-1 and r of this warp are bitwise
     // equal and uniform across the warp (and wet), every face touching row r-1
@@ -534,21 +563,21 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     // identity and the shared-memory march state is already correct; the row
     // is stored unchanged and its CFL speed comes from a one-entry cache.  The
     // result is bit-identical to the full path (tests: SILT_QUIET_SKIP=0).
-    __shared__ long long sh_cprev[4][kStepThreads];   // previous row (bits)
     // Speeds of the current quiescent streak (the state is the same on every
     // skipped row of a streak), folded into the reduction once per streak.
     bool quiet_prev = false, qvalid = false;
     double qsx = 0.0, qsy = 0.0;
 #pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
-        const int ahead = buf == 0 ? 2 : buf - 1;  // slot of row r+2
-        if (r + 2 <= je) prefetch_row(A, src, p, r + 2, row_sa0 + ahead * kSlotBytes);
+        const int ahead = buf == 0 ? SILT_RING - 1 : buf - 1;  // slot of row r+RING-1
+        if (r + SILT_RING - 1 <= je)
+            prefetch_row(A, src, p, r + SILT_RING - 1, row_sa0 + ahead * kSlotBytes);
         cp_async_commit();
-        cp_async_wait2();  // row r landed; rows r+1, r+2 may be in flight
+        cp_async_wait_ring();  // row r landed; the later rows may be in flight
         double c[4];
 #pragma unroll
         for (int f = 0; f < 4; ++f) c[f] = sh_row[buf][f][t];
-        buf = buf == 2 ? 0 : buf + 1;
+        buf = buf == SILT_RING - 1 ? 0 : buf + 1;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
 
@@ -766,9 +795,17 @@ __global__ void face_batch_kernel(Params P, const double* L, const double* Rr, l
 // Explicit instantiation hooks, defined by each TU with its own S.
 #define SILT_DEFINE_LAUNCHERS(S, NAME)                                                          \
     void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st) {                    \
-        if (A.dim == 2)                                                                          \
-            silt_dev::step2d_kernel<S><<<grid, kStepThreads, 0, st>>>(A, li);                    \
-        else                                                                                     \
+        if (A.dim == 2) {                                                                        \
+            static bool attr_set = false;                                                        \
+            if (!attr_set) {                                                                     \
+                cudaFuncSetAttribute(silt_dev::step2d_kernel<S>,                                 \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                                     (int)sizeof(silt_dev::StepSmem));                           \
+                attr_set = true;                                                                 \
+            }                                                                                    \
+            silt_dev::step2d_kernel<S>                                                           \
+                <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);                 \
+        } else                                                                                   \
             silt_dev::step1d_kernel<S><<<grid, kStepThreads, 0, st>>>(A, li);                    \
     }                                                                                            \
     void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st) {                 \

@@ -246,6 +246,11 @@ class StripRunner:
 
     # ---- solver interface ----------------------------------------------------
     def upload_device(self, tensor):
+        # the tensor was produced on torch's current stream; the solver copies
+        # on its own stream, so order the two first
+        if tensor.is_cuda:
+            import torch
+            torch.cuda.current_stream(tensor.device).synchronize()
         self.solver.upload_device(tensor.data_ptr())
         if self.torch_stream is not None:
             self.torch_stream.synchronize()

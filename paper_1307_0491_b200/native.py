@@ -164,6 +164,8 @@ class Solver:
         check(self.L.silt_solver_upload(self.h, _dp(field)))
 
     def upload_device(self, ptr: int):
+        """Device AoS copy on the solver's stream.  The caller orders the
+        producer of ``ptr`` first (e.g. torch.cuda.current_stream().synchronize())."""
         check(self.L.silt_solver_upload_device(self.h, ptr))
 
     def download(self, out: np.ndarray | None = None) -> np.ndarray:

@@ -32,7 +32,9 @@ def strip_ms(p, full, j0, n, steps, warmup):
     s = native.Solver(p, strip, 0, abi.VARIANT_FAST)
     stream = torch.cuda.Stream()
     s.set_stream(stream.cuda_stream)
-    s.upload_device(full[j0:j0 + n].contiguous().data_ptr())
+    strip_rows = full[j0:j0 + n].contiguous()
+    torch.cuda.synchronize()  # order torch's producer before the solver's copy
+    s.upload_device(strip_rows.data_ptr())
     ex = s.exchange_ptrs()
     for ptr, row in ((ex.recv_south, j0 - 1), (ex.recv_north, j0 + n)):
         if ptr:  # freeze the neighbour rows at their initial values
