@@ -263,22 +263,26 @@ def main():
         del full
         torch.cuda.empty_cache()
         partition = balanced_partition(costs, world)
-        pilot = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
-        pilot.upload_device(device_initial_rows(args.workload, p, pilot.j0, pilot.nrows, device))
-        pilot.begin(max_steps=8)
-        pilot.step(3)
-        pilot.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(pilot.torch_stream)
-        pilot.solver.step(4)  # this strip alone (its step kernels)
-        e1.record(pilot.torch_stream)
-        torch.cuda.synchronize()
-        mine = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
-        times = [torch.zeros_like(mine) for _ in range(world)]
-        torch.distributed.all_gather(times, mine)
-        pilot.close()
-        partition = refine_partition(costs, partition, [float(x.item()) for x in times])
-        torch.cuda.empty_cache()
+        for _ in range(2):  # two measured refinements
+            pilot = StripRunner(p, world, rank, device=local, variant=variant,
+                                partition=partition)
+            pilot.upload_device(device_initial_rows(args.workload, p, pilot.j0, pilot.nrows,
+                                                    device))
+            pilot.begin(max_steps=8)
+            pilot.step(3)
+            pilot.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(pilot.torch_stream)
+            pilot.solver.step(4)  # this strip alone (its step kernels)
+            e1.record(pilot.torch_stream)
+            torch.cuda.synchronize()
+            mine = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+            times = [torch.zeros_like(mine) for _ in range(world)]
+            torch.distributed.all_gather(times, mine)
+            pilot.close()
+            partition = refine_partition(costs, partition, [float(x.item()) for x in times])
+            torch.cuda.empty_cache()
     runner = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
     j0, nrows = runner.j0, runner.nrows
     init = device_initial_rows(args.workload, p, j0, nrows, device)

@@ -66,7 +66,7 @@ def balanced_partition(row_cost, parts: int):
     return [(cuts[k], cuts[k + 1] - cuts[k]) for k in range(parts)]
 
 
-QUIET_COST = 1.0 / 7.3  # measured on C4 strips (tools/strip_times.py): quiescent vs active segment
+QUIET_COST = 1.0 / 10.0  # measured on C4 strips (tools/strip_times.py): quiescent vs active segment
 
 
 def row_costs(field, h_dry: float = 1e-8, seg: int = 30, halo: int = 32):

@@ -66,10 +66,12 @@ def main():
     out = {"workload": a.workload, "t1_ms": t1, "runs": []}
     for n in (2, 4, 8):
         bal = balanced_partition(costs, n)
-        bal_t = [strip_ms(p, full, j0, c, 4, 3) for j0, c in bal]  # the pilot
+        bal_t = [strip_ms(p, full, j0, c, 4, 3) for j0, c in bal]  # pilot 1
+        ref1 = refine_partition(costs, bal, bal_t)
+        ref1_t = [strip_ms(p, full, j0, c, 4, 3) for j0, c in ref1]  # pilot 2
         for name, part in (("uniform", [block_range(p.ny, n, r) for r in range(n)]),
                            ("balanced", bal),
-                           ("refined", refine_partition(costs, bal, bal_t))):
+                           ("refined", refine_partition(costs, ref1, ref1_t))):
             ts = [strip_ms(p, full, j0, c, a.steps, a.warmup) for j0, c in part]
             eff = t1 / (n * max(ts))
             out["runs"].append({"n": n, "partition": name, "rows": [c for _, c in part],
