@@ -4,3 +4,14 @@
 
 SILT_DEFINE_LAUNCHERS(false, silt_fast)
 
+
+#ifdef SILT_STATS
+// diagnostics build only: read and reset the solver counters
+extern "C" int silt_debug_stats(unsigned long long* out, int n) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, silt_dev::g_stats, sizeof(unsigned long long) * (n < 8 ? n : 8));
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(silt_dev::g_stats, z, sizeof z);
+    return 0;
+}
+#endif

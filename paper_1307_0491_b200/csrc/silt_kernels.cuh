@@ -594,14 +594,21 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                     sh_cprev[f][t] = cb[f];
                 }
                 const bool eqy = r > jb - 1 && dif == 0ull;
-                const bool wet = c[0] > A.P.h_dry;
-                bool quiet = __all_sync(0xffffffffu, !owned || (eqy && wet));
-                if (quiet) {
-                    unsigned long long difx = 0;
+                // Inside a streak one vote suffices: if every lane (halo and
+                // dead lanes included) sees row r equal to row r-1, and row r-1
+                // was verified uniform across the warp and wet, so is row r.
+                bool quiet = quiet_prev && __all_sync(0xffffffffu, eqy);
+                if (!quiet) {
+                    const bool wet = c[0] > A.P.h_dry;
+                    quiet = __all_sync(0xffffffffu, !owned || (eqy && wet));
+                    if (quiet) {
+                        unsigned long long difx = 0;
 #pragma unroll
-                    for (int f = 0; f < 4; ++f)  // every lane shuffles
-                        difx |= (unsigned long long)(cb[f] ^ __shfl_down_sync(0xffffffffu, cb[f], 1));
-                    quiet = __all_sync(0xffffffffu, !xface || (difx == 0ull && wet));
+                        for (int f = 0; f < 4; ++f)  // every lane shuffles
+                            difx |= (unsigned long long)(cb[f] ^
+                                                         __shfl_down_sync(0xffffffffu, cb[f], 1));
+                        quiet = __all_sync(0xffffffffu, !xface || (difx == 0ull && wet));
+                    }
                 }
                 const bool skip = quiet && quiet_prev && r - 1 >= jb;
                 quiet_prev = quiet;

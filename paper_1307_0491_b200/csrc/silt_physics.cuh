@@ -19,6 +19,10 @@
 
 namespace silt_dev {
 
+#ifdef SILT_STATS
+__device__ unsigned long long g_stats[8];
+#endif
+
 // ---- constants (src/bedload.cpp:11, src/riemann.cpp:42-45) --------------
 constexpr double kUEps = 1e-10;
 constexpr double kSuppressB = 1e-12;
@@ -608,6 +612,12 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
         if (!accepted) return kTry ? kBail : kIllPosed;
     }
 
+#ifdef SILT_STATS
+    atomicAdd(&g_stats[0], 1ull);                       // fluid-outer solves
+    atomicAdd(&g_stats[1], (unsigned long long)it);     // Newton iterations
+    if (it == 0) atomicAdd(&g_stats[2], 1ull);          // converged at the guess
+    if (early) atomicAdd(&g_stats[3], 1ull);            // early-accepted
+#endif
     const double ustar = 0.5 * (m2 + m4 - b * c.kappa);
     const double wstar = l.omega + m2 * e.dzl;
     const double a2 = a * a;
