@@ -1,6 +1,7 @@
 /*
  * silt_cuda.h — C ABI of the B200-native time-stepping path for the coupled
- * shallow-water + Exner (Grass bedload) relaxation solver of arXiv 1307.0491.
+ * shallow-water + Exner (Grass or Shields-threshold bedload) relaxation solver
+ * of arXiv 1307.0491.
  *
  * This is the drop-in boundary.  Every entry point takes plain pointers and
  * sizes; nothing here mentions torch, std::vector or CUDA types (streams are
@@ -37,6 +38,8 @@
  *   silt_riemann_batch ............. equilibrate + celerity_bounds +
  *                                    interface_riemann (relax_state.hpp:27-51,
  *                                    riemann.hpp:33-35)
+ *   silt_law_batch ................. normal_flux + normal_flux_derivative
+ *                                    (include/silt/bedload.hpp:95-98)
  */
 #ifndef SILT_CUDA_H
 #define SILT_CUDA_H
@@ -48,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SILT_ABI_VERSION 1
+#define SILT_ABI_VERSION 2
 
 /* Status codes.  INVALID ~ std::invalid_argument, RUNTIME ~ std::runtime_error
  * in the reference (SURVEY §8b "Errors"). */
@@ -70,13 +73,31 @@ enum {
     SILT_BC_GIVEN = 4
 };
 
+/* BedloadLaw::Kind (include/silt/bedload.hpp:33). */
+enum { SILT_LAW_GRASS = 0, SILT_LAW_SHIELDS = 1 };
+
+/* ShieldsFormula, in the reference's enum order (include/silt/bedload.hpp:12-18). */
+enum {
+    SILT_SHIELDS_MPM = 0,       /* MeyerPeterMuller */
+    SILT_SHIELDS_FLVB = 1,      /* FernandezLuqueVanBeek */
+    SILT_SHIELDS_NIELSEN = 2,   /* Nielsen */
+    SILT_SHIELDS_RIBBERINK = 3, /* Ribberink */
+    SILT_SHIELDS_CAMENEN = 4    /* CamenenLarson */
+};
+
+/* FrictionModel (include/silt/bedload.hpp:20-23). */
+enum { SILT_FRICTION_DARCY_WEISBACH = 0, SILT_FRICTION_MANNING = 1 };
+
 /* Side order of Scenario::bc (include/silt/scenarios.hpp:15). */
 enum { SILT_WEST = 0, SILT_EAST = 1, SILT_SOUTH = 2, SILT_NORTH = 3 };
 
 /* Numerical variant of the kernels. FAST: contracted FMAs, reciprocals,
  * closed-form Grass terms; parity to 1e-9 normwise.  STRICT: the reference's
  * operation order, no FMA contraction, IEEE division and glibc's hypot
- * algorithm (bitwise-identical to the CPU reference). */
+ * algorithm (bitwise-identical to the CPU reference for the Grass law and for
+ * the Shields laws that need only sqrt: Darcy-Weisbach friction with MPM,
+ * FLVB or Nielsen; Manning friction and the Ribberink / Camenen formulas call
+ * pow/exp, where CUDA's libm may differ from glibc's by an ulp or two). */
 enum { SILT_VARIANT_FAST = 0, SILT_VARIANT_STRICT = 1 };
 
 /* Run state reported by silt_solver_status. */
@@ -94,15 +115,23 @@ typedef struct silt_bc {
     double h0;             /* Inflow (supercritical): imposed depth */
 } silt_bc;
 
-/* One configured problem: grid + physics + Grass law + BCs + run knobs. */
+/* One configured problem: grid + physics + bedload law + BCs + run knobs.
+ * The law fields mirror BedloadLaw (include/silt/bedload.hpp:32-52) and are
+ * validated like BedloadLaw::grass / BedloadLaw::shields (src/bedload.cpp:26-57). */
 typedef struct silt_problem {
     int32_t dim;       /* 1 or 2 */
     int32_t nx, ny;    /* global cell counts (ny == 1 in 1D) */
-    int32_t law_kind;  /* 0 = Grass; anything else is rejected (Shields out of scope) */
+    int32_t law_kind;  /* SILT_LAW_GRASS or SILT_LAW_SHIELDS */
     double dx, dy;     /* Grid::dx, Grid::dy (1D: dy = 1) */
     double gravity;    /* Physics::gravity */
     double h_dry;      /* Physics::h_dry */
-    double a_g, m_g;   /* BedloadLaw::grass(a_g, m_g) */
+    double a_g, m_g;   /* Grass: BedloadLaw::grass(a_g, m_g) */
+    int32_t shields_formula; /* Shields: SILT_SHIELDS_* */
+    int32_t friction_model;  /* Shields: SILT_FRICTION_* */
+    double tau_cr;           /* Shields: critical Shields stress (>= 0) */
+    double grain_diameter;   /* Shields: d_s (> 0) */
+    double rel_density;      /* Shields: s (> 1) */
+    double friction_coef;    /* Shields: Darcy f or Manning n (> 0) */
     double cfl;        /* Scenario::cfl, in (0, 1] */
     double safety;     /* Scenario::safety (>= 1) */
     silt_bc bc[4];     /* West, East, South, North */
@@ -231,6 +260,13 @@ int silt_step_padded(const silt_problem* problem, double* padded_aos,
 int silt_riemann_batch(const silt_problem* problem, const double* left,
                        const double* right, int64_t n, int axis, int variant,
                        double* out);
+
+/* Batch of bedload-law evaluations as the step kernels make them: states[n][3]
+ * = {h, u_n, u_t}; out[n][2] = {normal_flux(law, h, u_n, u_t, g),
+ * normal_flux_derivative(law, h, u_n, u_t, g)} (src/bedload.cpp:207-223),
+ * for either law kind.  Host arrays. */
+int silt_law_batch(const silt_problem* problem, const double* states, int64_t n,
+                   int variant, double* out);
 
 /* Device math self-test (diagnostics): for k < n,
  *   out[4k+0] = FAST reciprocal of x[k]      out[4k+1] = IEEE 1/x[k]

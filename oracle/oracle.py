@@ -81,6 +81,12 @@ class CpuSolver:
         g = getattr(L, f"{prefix}_relax")
         g.argtypes = [_P, _D, _D, C.c_int, _D]
         self._relax = g
+        g = getattr(L, f"{prefix}_law_eval")
+        g.argtypes = [_P, _D, _I64, _D]
+        self._law = g
+        g = getattr(L, f"{prefix}_shields_flux")
+        g.argtypes = [C.c_int, _D, _D, _I64, _D]
+        self._shields = g
         if prefix == "ref":
             g = L.ref_run_parallel
             g.argtypes = [_P, _D, C.c_double, _I64, C.c_int, C.c_int, _D,
@@ -158,6 +164,22 @@ class CpuSolver:
         rc = np.ascontiguousarray(rc, dtype=np.float64)
         out = np.empty(12)
         self._check(self._relax(C.byref(problem), _dp(lc), _dp(rc), axis, _dp(out)))
+        return out
+
+    def law_eval(self, problem, states) -> np.ndarray:
+        """(n, 6) law probes of states (n, 3) = (h, u_n, u_t): dimensional_flux,
+        dqs_du, normal_flux, normal_flux_derivative, shields_stress, friction_slope."""
+        states = np.ascontiguousarray(states, dtype=np.float64).reshape(-1, 3)
+        out = np.empty((states.shape[0], 6))
+        self._check(self._law(C.byref(problem), _dp(states), states.shape[0], _dp(out)))
+        return out
+
+    def shields_flux(self, formula: int, tau, tau_cr) -> np.ndarray:
+        """(n, 2): shields_flux, shields_flux_derivative."""
+        tau = np.ascontiguousarray(tau, dtype=np.float64).ravel()
+        tau_cr = np.ascontiguousarray(np.broadcast_to(tau_cr, tau.shape), dtype=np.float64)
+        out = np.empty((tau.size, 2))
+        self._check(self._shields(formula, _dp(tau), _dp(tau_cr), tau.size, _dp(out)))
         return out
 
 

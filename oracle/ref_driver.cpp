@@ -104,12 +104,27 @@ void store_field(const Field& f, double* aos) {
     }
 }
 
+// BedloadLaw from the ABI problem, through the reference's own factories
+// (src/bedload.cpp:26-57) so their validation applies.
+BedloadLaw make_law(const silt_problem& p) {
+    if (p.law_kind == SILT_LAW_GRASS) return BedloadLaw::grass(p.a_g, p.m_g);
+    if (p.law_kind != SILT_LAW_SHIELDS) throw std::invalid_argument("bedload: unknown law kind");
+    if (p.shields_formula < 0 || p.shields_formula > 4)
+        throw std::invalid_argument("bedload: unknown Shields formula");
+    FrictionLaw fric;
+    fric.model = p.friction_model == SILT_FRICTION_MANNING ? FrictionModel::Manning
+                                                           : FrictionModel::DarcyWeisbach;
+    fric.coefficient = p.friction_coef;
+    return BedloadLaw::shields(static_cast<ShieldsFormula>(p.shields_formula), fric, p.tau_cr,
+                               p.grain_diameter, p.rel_density);
+}
+
 Scenario make_scenario(const silt_problem& p, const double* init, double t_end) {
     Scenario sc;
     sc.name = "oracle";
     sc.grid = make_grid(p);
     sc.initial = make_field(sc.grid, init);
-    sc.law = BedloadLaw::grass(p.a_g, p.m_g);
+    sc.law = make_law(p);
     sc.phys = make_phys(p);
     for (int s = 0; s < 4; ++s) sc.bc[s] = make_bc(p.bc[s]);
     sc.t_end = t_end;
@@ -191,7 +206,7 @@ int ref_run_parallel(const silt_problem* p, const double* init, double t_end,
 int ref_cfl_dt(const silt_problem* p, const double* field, double* dt) {
     return guarded([&] {
         const Field f = make_field(make_grid(*p), field);
-        *dt = cfl_dt(f, BedloadLaw::grass(p->a_g, p->m_g), make_phys(*p), p->cfl);
+        *dt = cfl_dt(f, make_law(*p), make_phys(*p), p->cfl);
     });
 }
 
@@ -203,7 +218,7 @@ int ref_step_padded(const silt_problem* p, double* padded, double dt) {
         for (std::size_t k = 0; k < n; ++k)
             f.cells[k] = {padded[4 * k], padded[4 * k + 1], padded[4 * k + 2],
                           padded[4 * k + 3]};
-        const BedloadLaw law = BedloadLaw::grass(p->a_g, p->m_g);
+        const BedloadLaw law = make_law(*p);
         if (p->dim == 1)
             step_1d(f, law, make_phys(*p), dt, p->safety);
         else
@@ -242,7 +257,7 @@ int ref_apply_bcs(const silt_problem* p, double* padded) {
 int ref_face_batch(const silt_problem* p, const double* L, const double* R,
                    int64_t n, int axis, double* out, double* info) {
     return guarded([&] {
-        const BedloadLaw law = BedloadLaw::grass(p->a_g, p->m_g);
+        const BedloadLaw law = make_law(*p);
         const Physics phys = make_phys(*p);
         const Axis ax = axis == 0 ? Axis::X : Axis::Y;
         for (int64_t k = 0; k < n; ++k) {
@@ -309,7 +324,7 @@ int ref_riemann(const double* l5, const double* r5, double a, double b, double g
 int ref_relax(const silt_problem* p, const double* lc4, const double* rc4, int axis,
               double* out) {
     return guarded([&] {
-        const BedloadLaw law = BedloadLaw::grass(p->a_g, p->m_g);
+        const BedloadLaw law = make_law(*p);
         const Physics phys = make_phys(*p);
         const Axis ax = axis == 0 ? Axis::X : Axis::Y;
         const FlowState lc{lc4[0], lc4[1], lc4[2], lc4[3]};
@@ -331,6 +346,39 @@ int ref_relax(const silt_problem* p, const double* lc4, const double* rc4, int a
         }
         out[10] = c.a;
         out[11] = c.b;
+    });
+}
+
+// Law probes (states[n][3] = h, u_n, u_t).  out[n][6] = {dimensional_flux(h,
+// u_n), flux_derivatives(h, h u_n).dqs_du, normal_flux, normal_flux_derivative,
+// shields_stress(h, u_n) (0 for Grass), friction_slope(u_n, h) (0 for Grass)}.
+int ref_law_eval(const silt_problem* p, const double* X, int64_t n, double* out) {
+    return guarded([&] {
+        const BedloadLaw law = make_law(*p);
+        const double g = p->gravity;
+        const bool sh = law.kind == BedloadLaw::Kind::Shields;
+        for (int64_t k = 0; k < n; ++k) {
+            const double h = X[3 * k], un = X[3 * k + 1], ut = X[3 * k + 2];
+            double* o = out + 6 * k;
+            o[0] = dimensional_flux(law, h, un, g);
+            o[1] = flux_derivatives(law, h, h * un, g).dqs_du;
+            o[2] = normal_flux(law, h, un, ut, g);
+            o[3] = normal_flux_derivative(law, h, un, ut, g);
+            o[4] = sh ? shields_stress(law, h, un, g) : 0.0;
+            o[5] = sh ? friction_slope(law.friction, un, h, g) : 0.0;
+        }
+    });
+}
+
+// out[n][2] = {shields_flux, shields_flux_derivative}(formula, tau[k], tau_cr[k])
+int ref_shields_flux(int formula, const double* tau, const double* tau_cr, int64_t n,
+                     double* out) {
+    return guarded([&] {
+        const ShieldsFormula f = static_cast<ShieldsFormula>(formula);
+        for (int64_t k = 0; k < n; ++k) {
+            out[2 * k] = shields_flux(f, tau[k], tau_cr[k]);
+            out[2 * k + 1] = shields_flux_derivative(f, tau[k], tau_cr[k]);
+        }
     });
 }
 

@@ -2,7 +2,8 @@
  * oracle/silt_oracle.c — TEST INFRASTRUCTURE ONLY (the parity checker).
  *
  * A plain-C11 restatement of the reference's time-stepping path for the
- * coupled shallow-water + Exner (Grass) relaxation scheme of arXiv 1307.0491.
+ * coupled shallow-water + Exner relaxation scheme of arXiv 1307.0491 (Grass
+ * and Shields-threshold bedload closures).
  * Every function follows the reference operation by operation (same operand
  * order, no FMA contraction: built with -ffp-contract=off) so that it agrees
  * bit for bit with the reference compiled with its Release flags; the tests
@@ -56,8 +57,17 @@ static prim_t primitives(cell_t s, double h_dry) {
 /* RelaxState::u (include/silt/relax_state.hpp:20) */
 static double relax_u(const relax_t* s, double h_dry) { return s->h > h_dry ? s->hu / s->h : 0.0; }
 
-/* ---- Grass closure: src/bedload.cpp ------------------------------------- */
+/* ---- bedload closures: src/bedload.cpp ---------------------------------- */
 #define K_UEPS 1e-10 /* src/bedload.cpp:11 */
+
+/* BedloadLaw (include/silt/bedload.hpp:32-52) + Physics::gravity */
+typedef struct {
+    double gravity, h_dry;
+    int kind;                  /* 0 Grass, 1 Shields */
+    double a_g, m_g;           /* Grass */
+    int formula, friction;     /* Shields: ShieldsFormula, FrictionModel (0 DW, 1 Manning) */
+    double tau_cr, d_s, rel_density, fcoef;
+} phys_t;
 
 /* abs_pow: src/bedload.cpp:14-20 */
 static double abs_pow(double au, double p) {
@@ -68,41 +78,116 @@ static double abs_pow(double au, double p) {
     return pow(au, p);
 }
 
+/* positive_part: src/bedload.cpp:22 */
+static double positive_part(double x) { return x > 0 ? x : 0.0; }
+
 /* grass_flux: src/bedload.cpp:78-80 */
 static double grass_flux(double u, double a_g, double m_g) {
     return a_g * u * abs_pow(fabs(u), m_g - 1.0);
 }
 
-/* flux_derivatives(...).dqs_du, Grass branch: src/bedload.cpp:165-177 */
-static double grass_dqs_du(double a_g, double m_g, double h, double hu) {
+/* friction_slope: src/bedload.cpp:82-92 */
+static double friction_slope(const phys_t* P, double u, double h) {
     if (!(h > 0)) return 0.0;
-    const double u = hu / h;
-    return a_g * m_g * abs_pow(fabs(u), m_g - 1.0);
+    const double drag = u * fabs(u);
+    if (P->friction == 0) return P->fcoef * drag / (8.0 * P->gravity * h);
+    return P->fcoef * P->fcoef * drag / pow(h, 4.0 / 3.0);
 }
 
-/* normal_flux: src/bedload.cpp:207-213 (dimensional_flux == grass_flux, :155-156) */
-static double normal_flux(double a_g, double m_g, double h, double un, double ut) {
-    (void)h;
+/* shields_flux: src/bedload.cpp:94-116 */
+static double shields_flux(int formula, double tau, double tau_cr) {
+    double e;
+    switch (formula) {
+        case 0: e = positive_part(tau - tau_cr); return 8.0 * e * sqrt(e);
+        case 1: e = positive_part(tau - tau_cr); return 5.7 * e * sqrt(e);
+        case 2:
+            if (tau <= 0) return 0.0;
+            return 12.0 * sqrt(tau) * positive_part(tau - tau_cr);
+        case 3: return 11.0 * pow(positive_part(tau - tau_cr), 1.65);
+        case 4:
+            if (tau <= 0) return 0.0;
+            return 12.0 * tau * sqrt(tau) * exp(-4.5 * tau_cr / tau);
+    }
+    return 0.0;
+}
+
+/* shields_flux_derivative: src/bedload.cpp:118-147 */
+static double shields_flux_derivative(int formula, double tau, double tau_cr) {
+    double rt;
+    switch (formula) {
+        case 0:
+            if (tau < tau_cr) return 0.0;
+            return 12.0 * sqrt(tau - tau_cr);
+        case 1:
+            if (tau < tau_cr) return 0.0;
+            return 8.55 * sqrt(tau - tau_cr);
+        case 2:
+            if (tau <= 0 || tau < tau_cr) return 0.0;
+            rt = sqrt(tau);
+            return 6.0 * (tau - tau_cr) / rt + 12.0 * rt;
+        case 3:
+            if (tau < tau_cr) return 0.0;
+            return 11.0 * 1.65 * pow(positive_part(tau - tau_cr), 0.65);
+        case 4:
+            if (tau <= 0) return 0.0;
+            rt = sqrt(tau);
+            return 12.0 * exp(-4.5 * tau_cr / tau) * (1.5 * rt + 4.5 * tau_cr / rt);
+    }
+    return 0.0;
+}
+
+/* shields_stress: src/bedload.cpp:149-153 */
+static double shields_stress(const phys_t* P, double h, double u) {
+    if (!(h > 0)) return 0.0;
+    const double sf = friction_slope(P, fabs(u), h);
+    return h * sf / ((P->rel_density - 1.0) * P->d_s);
+}
+
+/* dimensional_flux: src/bedload.cpp:155-163 */
+static double dimensional_flux(const phys_t* P, double h, double u) {
+    if (P->kind == 0) return grass_flux(u, P->a_g, P->m_g);
+    if (!(h > 0) || fabs(u) <= K_UEPS) return 0.0;
+    const double tau = shields_stress(P, h, u);
+    const double qstar = shields_flux(P->formula, tau, P->tau_cr);
+    const double d = P->d_s;
+    const double scale = sqrt((P->rel_density - 1.0) * P->gravity * d * d * d);
+    return copysign(qstar * scale, u);
+}
+
+/* flux_derivatives(...).dqs_du: src/bedload.cpp:165-200 */
+static double dqs_du(const phys_t* P, double h, double hu) {
+    if (!(h > 0)) return 0.0;
+    const double u = hu / h;
+    if (P->kind == 0) return P->a_g * P->m_g * abs_pow(fabs(u), P->m_g - 1.0);
+    if (fabs(u) <= K_UEPS) return 0.0;
+    const double tau = shields_stress(P, h, u);
+    const double dqstar = shields_flux_derivative(P->formula, tau, P->tau_cr);
+    if (dqstar == 0.0) return 0.0;
+    const double ds = P->d_s;
+    const double scale = sqrt((P->rel_density - 1.0) * P->gravity * ds * ds * ds);
+    const double dtau_du = 2.0 * tau / u;
+    const double sgn = (u > 0) ? 1.0 : -1.0;
+    return sgn * scale * dqstar * dtau_du;
+}
+
+/* normal_flux: src/bedload.cpp:207-213 */
+static double normal_flux(const phys_t* P, double h, double un, double ut) {
     const double speed = hypot(un, ut);
     if (speed <= K_UEPS) return 0.0;
-    return grass_flux(speed, a_g, m_g) * (un / speed);
+    return dimensional_flux(P, h, speed) * (un / speed);
 }
 
 /* normal_flux_derivative: src/bedload.cpp:215-223 */
-static double normal_flux_derivative(double a_g, double m_g, double h, double un, double ut) {
+static double normal_flux_derivative(const phys_t* P, double h, double un, double ut) {
     const double speed = hypot(un, ut);
     if (speed <= K_UEPS) return 0.0;
-    const double rate = grass_flux(speed, a_g, m_g);
-    const double drate = grass_dqs_du(a_g, m_g, h, h * speed);
+    const double rate = dimensional_flux(P, h, speed);
+    const double drate = dqs_du(P, h, h * speed);
     const double ratio = un / speed;
     return rate / speed + ratio * ratio * (drate - rate / speed);
 }
 
 /* ---- relaxation state + celerities: src/relax_state.cpp ----------------- */
-typedef struct {
-    double gravity, h_dry, a_g, m_g;
-} phys_t;
-
 /* equilibrate: src/relax_state.cpp:8-21 */
 static relax_t equilibrate(cell_t cell, const phys_t* P, int axis) {
     const prim_t p = primitives(cell, P->h_dry);
@@ -113,7 +198,7 @@ static relax_t equilibrate(cell_t cell, const phys_t* P, int axis) {
     s.hu = cell.h * un;
     s.pi = 0.5 * P->gravity * cell.h * cell.h;
     s.z = cell.zb;
-    s.omega = normal_flux(P->a_g, P->m_g, cell.h, un, ut);
+    s.omega = normal_flux(P, cell.h, un, ut);
     return s;
 }
 
@@ -135,10 +220,10 @@ static void celerity_bounds(const relax_t* l, const relax_t* r, double ut_l, dou
         const double un = relax_u(s, P->h_dry);
         const double ut = k == 0 ? ut_l : ut_r;
         a = dmax(a, s->h * sqrt(g * s->h));
-        const double dq = normal_flux_derivative(P->a_g, P->m_g, s->h, un, ut);
+        const double dq = normal_flux_derivative(P, s->h, un, ut);
         b2 = dmax(b2, s->hu * s->hu + g * s->h * s->h * dq);
         const double speed = hypot(un, ut);
-        if (grass_flux(speed, P->a_g, P->m_g) != 0.0 || dq != 0.0 || s->omega != 0.0) still = 0;
+        if (dimensional_flux(P, s->h, speed) != 0.0 || dq != 0.0 || s->omega != 0.0) still = 0;
     }
     *a_out = safety * a;
     *b_out = still ? 0.0 : safety * sqrt(b2);
@@ -484,7 +569,7 @@ static const char* kNegDepth =
 /* axis_speed: src/stepper.cpp:30-36 */
 static double axis_speed(const phys_t* P, double h, double un, double ut) {
     const double fluid = fabs(un) + sqrt(P->gravity * h);
-    const double dq = normal_flux_derivative(P->a_g, P->m_g, h, un, ut);
+    const double dq = normal_flux_derivative(P, h, un, ut);
     const double solid = fabs(un) + sqrt(un * un + P->gravity * dq);
     return dmax(fluid, solid);
 }
@@ -506,8 +591,15 @@ static grid_t make_grid(const silt_problem* p) {
     g.dy = p->dim == 1 ? 1.0 : p->dy;
     g.P.gravity = p->gravity;
     g.P.h_dry = p->h_dry;
+    g.P.kind = p->law_kind;
     g.P.a_g = p->a_g;
     g.P.m_g = p->m_g;
+    g.P.formula = p->shields_formula;
+    g.P.friction = p->friction_model;
+    g.P.tau_cr = p->tau_cr;
+    g.P.d_s = p->grain_diameter;
+    g.P.rel_density = p->rel_density;
+    g.P.fcoef = p->friction_coef;
     g.cfl = p->cfl;
     g.safety = p->safety;
     memcpy(g.bc, p->bc, sizeof g.bc);
@@ -714,11 +806,33 @@ static int cmp_double(const void* a, const void* b) {
     return (x > y) - (x < y);
 }
 
+/* BedloadLaw::grass / BedloadLaw::shields validation: src/bedload.cpp:26-57 */
+static int check_law(const silt_problem* p) {
+    if (p->law_kind == 0) {
+        if (!(p->a_g >= 0) || !isfinite(p->a_g))
+            return set_err(SILT_ERR_INVALID, "bedload: Grass a_g must be >= 0");
+        if (!(p->m_g >= 1.0 && p->m_g <= 4.0))
+            return set_err(SILT_ERR_INVALID, "bedload: Grass m_g must lie in [1, 4]");
+        return 0;
+    }
+    if (p->law_kind != 1 || p->shields_formula < 0 || p->shields_formula > 4 ||
+        p->friction_model < 0 || p->friction_model > 1)
+        return set_err(SILT_ERR_INVALID, "bedload: unknown law");
+    if (!(p->tau_cr >= 0)) return set_err(SILT_ERR_INVALID, "bedload: tau_cr must be >= 0");
+    if (!(p->grain_diameter > 0))
+        return set_err(SILT_ERR_INVALID, "bedload: grain diameter must be > 0");
+    if (!(p->rel_density > 1))
+        return set_err(SILT_ERR_INVALID, "bedload: relative density must exceed 1");
+    if (!(p->friction_coef > 0))
+        return set_err(SILT_ERR_INVALID, "bedload: friction coefficient must be > 0");
+    return 0;
+}
+
 /* run_serial loop: src/parallel.cpp:208-259 (make_plan :101-127, next_stop :129-132) */
 int orc_run(const silt_problem* p, const double* init, double t_end, int64_t max_steps,
             const double* snaps, int n_snaps, double* out, double* dt_log, int64_t dt_cap,
             int64_t* steps_out, double* t_out) {
-    if (p->law_kind != 0) return set_err(SILT_ERR_UNSUPPORTED, "only the Grass law is restated");
+    if (check_law(p)) return SILT_ERR_INVALID;
     if (!(t_end >= 0)) return set_err(SILT_ERR_INVALID, "run: t_end must be >= 0");
     const grid_t g = make_grid(p);
     double* plan = (double*)malloc(sizeof(double) * (size_t)(n_snaps > 0 ? n_snaps : 1));
@@ -864,4 +978,31 @@ int orc_relax(const silt_problem* p, const double* lc4, const double* rc4, int a
     out[10] = a;
     out[11] = b;
     return SILT_OK;
+}
+
+/* Law probes, same layout as ref_law_eval (oracle/ref_driver.cpp). */
+int orc_law_eval(const silt_problem* p, const double* X, int64_t n, double* out) {
+    if (check_law(p)) return SILT_ERR_INVALID;
+    const grid_t g = make_grid(p);
+    const phys_t* P = &g.P;
+    for (int64_t k = 0; k < n; ++k) {
+        const double h = X[3 * k], un = X[3 * k + 1], ut = X[3 * k + 2];
+        double* o = out + 6 * k;
+        o[0] = dimensional_flux(P, h, un);
+        o[1] = dqs_du(P, h, h * un);
+        o[2] = normal_flux(P, h, un, ut);
+        o[3] = normal_flux_derivative(P, h, un, ut);
+        o[4] = P->kind == 1 ? shields_stress(P, h, un) : 0.0;
+        o[5] = P->kind == 1 ? friction_slope(P, un, h) : 0.0;
+    }
+    return 0;
+}
+
+int orc_shields_flux(int formula, const double* tau, const double* tau_cr, int64_t n,
+                     double* out) {
+    for (int64_t k = 0; k < n; ++k) {
+        out[2 * k] = shields_flux(formula, tau[k], tau_cr[k]);
+        out[2 * k + 1] = shields_flux_derivative(formula, tau[k], tau_cr[k]);
+    }
+    return 0;
 }

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 
-SILT_ABI_VERSION = 1
+SILT_ABI_VERSION = 2
 
 SILT_OK = 0
 SILT_ERR_INVALID = 1
@@ -28,6 +28,15 @@ WEST, EAST, SOUTH, NORTH = 0, 1, 2, 3
 VARIANT_FAST = 0
 VARIANT_STRICT = 1
 
+LAW_GRASS = 0
+LAW_SHIELDS = 1
+
+# ShieldsFormula / FrictionModel in the reference's enum order
+# (include/silt/bedload.hpp:12-23); keys are the reference's CLI/config names
+# (src/config.cpp:228-267).
+SHIELDS_FORMULAS = {"mpm": 0, "flvb": 1, "nielsen": 2, "ribberink": 3, "camenen": 4}
+FRICTION_MODELS = {"darcy-weisbach": 0, "manning": 1}
+
 STATE_RUNNING = 0
 STATE_DONE = 1
 STATE_PAUSED = 2
@@ -45,6 +54,9 @@ class SiltProblem(C.Structure):
                 ("dx", C.c_double), ("dy", C.c_double),
                 ("gravity", C.c_double), ("h_dry", C.c_double),
                 ("a_g", C.c_double), ("m_g", C.c_double),
+                ("shields_formula", C.c_int32), ("friction_model", C.c_int32),
+                ("tau_cr", C.c_double), ("grain_diameter", C.c_double),
+                ("rel_density", C.c_double), ("friction_coef", C.c_double),
                 ("cfl", C.c_double), ("safety", C.c_double),
                 ("bc", SiltBC * 4)]
 
@@ -101,6 +113,26 @@ def make_problem(dim: int, nx: int, ny: int, dx: float, dy: float, *,
     bcs = bcs or [bc("outflow")] * 4
     for s in range(4):
         p.bc[s] = bcs[s]
+    return p
+
+
+def set_shields(p: SiltProblem, formula: str = "mpm", friction: str = "manning",
+                friction_coef: float | None = None, tau_cr: float = 0.047,
+                grain_diameter: float = 1e-3, rel_density: float = 2.65) -> SiltProblem:
+    """Switch a problem to BedloadLaw::shields (reference src/bedload.cpp:38-57).
+
+    Defaults follow the reference's config layer (src/config.cpp:226-247):
+    Manning friction; coefficient 0.025 for Manning, 0.03 for Darcy-Weisbach.
+    """
+    p.law_kind = LAW_SHIELDS
+    p.shields_formula = SHIELDS_FORMULAS[formula]
+    p.friction_model = FRICTION_MODELS[friction]
+    if friction_coef is None:
+        friction_coef = 0.025 if friction == "manning" else 0.03
+    p.friction_coef = float(friction_coef)
+    p.tau_cr = float(tau_cr)
+    p.grain_diameter = float(grain_diameter)
+    p.rel_density = float(rel_density)
     return p
 
 

@@ -103,6 +103,36 @@ struct silt_solver {
 
 namespace {
 
+// Device parameters of a validated problem.  Shields constants are evaluated
+// in the reference's operation order (src/bedload.cpp:152, :161) so the STRICT
+// kernels see the same doubles.
+silt_dev::Params make_params(const silt_problem& p) {
+    silt_dev::Params P{};
+    P.g = p.gravity;
+    P.h_dry = p.h_dry;
+    P.a_g = p.a_g;
+    P.m_g = p.m_g;
+    P.safety = p.safety;
+    P.half_g = 0.5 * p.gravity;
+    P.m3 = p.m_g == 3.0;
+    P.shields = p.law_kind == SILT_LAW_SHIELDS;
+    if (P.shields) {
+        P.formula = p.shields_formula;
+        P.friction = p.friction_model;
+        P.tau_cr = p.tau_cr;
+        P.d_s = p.grain_diameter;
+        P.rel_density = p.rel_density;
+        P.fcoef = p.friction_coef;
+        const double d = p.grain_diameter;
+        P.scale = std::sqrt((p.rel_density - 1.0) * p.gravity * d * d * d);
+        const double sd = (p.rel_density - 1.0) * d;
+        P.ktau = p.friction_model == SILT_FRICTION_MANNING
+                     ? p.friction_coef * p.friction_coef / sd
+                     : p.friction_coef / (8.0 * p.gravity * sd);
+    }
+    return P;
+}
+
 int validate_problem(const silt_problem* p) {
     if (!p) return fail(SILT_ERR_INVALID, "silt: null problem");
     if (p->dim != 1 && p->dim != 2) return fail(SILT_ERR_INVALID, "grid: dim must be 1 or 2");
@@ -112,13 +142,27 @@ int validate_problem(const silt_problem* p) {
         return fail(SILT_ERR_INVALID, "grid: length_x must be positive");
     if (p->dim == 2 && (!(p->dy > 0) || !std::isfinite(p->dy)))
         return fail(SILT_ERR_INVALID, "grid: length_y must be positive");
-    if (p->law_kind != 0)
-        return fail(SILT_ERR_UNSUPPORTED,
-                    "bedload: only the Grass law is implemented on the GPU path");
-    if (!(p->a_g >= 0) || !std::isfinite(p->a_g))
-        return fail(SILT_ERR_INVALID, "bedload: Grass a_g must be >= 0");
-    if (!(p->m_g >= 1.0 && p->m_g <= 4.0))
-        return fail(SILT_ERR_INVALID, "bedload: Grass m_g must lie in [1, 4]");
+    if (p->law_kind == SILT_LAW_GRASS) {  // BedloadLaw::grass, src/bedload.cpp:26-36
+        if (!(p->a_g >= 0) || !std::isfinite(p->a_g))
+            return fail(SILT_ERR_INVALID, "bedload: Grass a_g must be >= 0");
+        if (!(p->m_g >= 1.0 && p->m_g <= 4.0))
+            return fail(SILT_ERR_INVALID, "bedload: Grass m_g must lie in [1, 4]");
+    } else if (p->law_kind == SILT_LAW_SHIELDS) {  // BedloadLaw::shields, :38-57
+        if (p->shields_formula < SILT_SHIELDS_MPM || p->shields_formula > SILT_SHIELDS_CAMENEN)
+            return fail(SILT_ERR_INVALID, "bedload: unknown Shields formula");
+        if (p->friction_model != SILT_FRICTION_DARCY_WEISBACH &&
+            p->friction_model != SILT_FRICTION_MANNING)
+            return fail(SILT_ERR_INVALID, "bedload: unknown friction model");
+        if (!(p->tau_cr >= 0)) return fail(SILT_ERR_INVALID, "bedload: tau_cr must be >= 0");
+        if (!(p->grain_diameter > 0))
+            return fail(SILT_ERR_INVALID, "bedload: grain diameter must be > 0");
+        if (!(p->rel_density > 1))
+            return fail(SILT_ERR_INVALID, "bedload: relative density must exceed 1");
+        if (!(p->friction_coef > 0))
+            return fail(SILT_ERR_INVALID, "bedload: friction coefficient must be > 0");
+    } else {
+        return fail(SILT_ERR_INVALID, "bedload: unknown law kind");
+    }
     const bool px0 = p->bc[SILT_WEST].type == SILT_BC_PERIODIC;
     const bool px1 = p->bc[SILT_EAST].type == SILT_BC_PERIODIC;
     if (px0 != px1) return fail(SILT_ERR_INVALID, "apply_bcs: periodic requires both x sides");
@@ -262,13 +306,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     A.dx = problem->dx;
     A.dy = problem->dim == 1 ? 1.0 : problem->dy;
     A.cfl = problem->cfl;
-    A.P.g = problem->gravity;
-    A.P.h_dry = problem->h_dry;
-    A.P.a_g = problem->a_g;
-    A.P.m_g = problem->m_g;
-    A.P.safety = problem->safety;
-    A.P.half_g = 0.5 * problem->gravity;
-    A.P.m3 = problem->m_g == 3.0;
+    A.P = make_params(*problem);
     for (int k = 0; k < 4; ++k) {
         A.bc_type[k] = problem->bc[k].type;
         A.bc_super[k] = problem->bc[k].supercritical;
@@ -902,14 +940,7 @@ int silt_riemann_batch(const silt_problem* problem, const double* left, const do
     if (int rc = validate_problem(problem)) return rc;
     if (n <= 0) return SILT_OK;
     CUDA_TRY(cudaSetDevice(0));
-    silt_dev::Params P;
-    P.g = problem->gravity;
-    P.h_dry = problem->h_dry;
-    P.a_g = problem->a_g;
-    P.m_g = problem->m_g;
-    P.safety = problem->safety;
-    P.half_g = 0.5 * problem->gravity;
-    P.m3 = problem->m_g == 3.0;
+    const silt_dev::Params P = make_params(*problem);
     double *dl = nullptr, *dr = nullptr, *dout = nullptr;
     unsigned* derr = nullptr;
     const size_t b4 = 4 * (size_t)n * sizeof(double), b5 = 5 * (size_t)n * sizeof(double);
@@ -936,6 +967,27 @@ int silt_riemann_batch(const silt_problem* problem, const double* left, const do
     if (herr)
         return fail(SILT_ERR_RUNTIME,
                     "interface_riemann: no positive fan after 25 celerity enlargements");
+    return SILT_OK;
+}
+
+int silt_law_batch(const silt_problem* problem, const double* states, int64_t n, int variant,
+                   double* out) {
+    if (int rc = validate_problem(problem)) return rc;
+    if (n <= 0) return SILT_OK;
+    CUDA_TRY(cudaSetDevice(0));
+    const silt_dev::Params P = make_params(*problem);
+    double *dx = nullptr, *dout = nullptr;
+    CUDA_TRY(cudaMalloc(&dx, 3 * (size_t)n * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dout, 2 * (size_t)n * sizeof(double)));
+    cudaMemcpy(dx, states, 3 * (size_t)n * sizeof(double), cudaMemcpyHostToDevice);
+    if (variant == SILT_VARIANT_STRICT)
+        silt_strict_law(P, dx, n, dout, 0);
+    else
+        silt_fast_law(P, dx, n, dout, 0);
+    cudaError_t e = cudaMemcpy(out, dout, 2 * (size_t)n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dout);
+    if (e != cudaSuccess) return fail(SILT_ERR_CUDA, cudaGetErrorString(e));
     return SILT_OK;
 }
 

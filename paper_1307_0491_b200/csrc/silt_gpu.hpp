@@ -14,9 +14,8 @@
 // Same argument meaning, same exception classes and messages:
 // std::invalid_argument for preconditions, std::runtime_error for numerical
 // failure (negative depth, no positive Riemann fan).  Differences, by design:
-//   * only the Grass law runs on the GPU; a Shields law throws
-//     std::invalid_argument ("bedload: only the Grass law is implemented on
-//     the GPU path") — there is no CPU fallback;
+//   * both law kinds (Grass, Shields x 5 formulas x 2 friction models) run on
+//     the GPU; there is no CPU fallback;
 //   * run_parallel(sc, px, py) validates px/py like partition() and runs py
 //     row strips (columns are never split: every layout is bitwise identical,
 //     tests/test_parallel.cpp:215-238), strip k on CUDA device k % devices;
@@ -60,7 +59,14 @@ inline silt_problem problem(const Grid& g, const BedloadLaw& law, const Physics&
     p.dim = g.dim;
     p.nx = g.nx;
     p.ny = g.dim == 1 ? 1 : g.ny;
-    p.law_kind = law.kind == BedloadLaw::Kind::Grass ? 0 : 1;
+    p.law_kind = law.kind == BedloadLaw::Kind::Grass ? SILT_LAW_GRASS : SILT_LAW_SHIELDS;
+    p.shields_formula = static_cast<int32_t>(law.formula);
+    p.friction_model = law.friction.model == FrictionModel::Manning ? SILT_FRICTION_MANNING
+                                                                    : SILT_FRICTION_DARCY_WEISBACH;
+    p.tau_cr = law.tau_cr;
+    p.grain_diameter = law.grain_diameter;
+    p.rel_density = law.rel_density;
+    p.friction_coef = law.friction.coefficient;
     p.dx = g.dx;
     p.dy = g.dim == 1 ? 1.0 : g.dy;
     p.gravity = phys.gravity;

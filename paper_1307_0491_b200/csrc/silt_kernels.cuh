@@ -262,26 +262,35 @@ __device__ __forceinline__ void write_edges(const StepArgs& A, int q, int col, i
 
 // Per-cell CFL candidates of a state (axis_speed, src/stepper.cpp:30-36, on
 // primitives of a wet cell).
-template <bool S>
+template <bool S, bool SH>
 __device__ __forceinline__ void cell_speeds(const StepArgs& A, const double c[4], double& sx,
                                             double& sy) {
     const Params& P = A.P;
     const double h = c[0];
     if constexpr (S) {
         const double u = c[1] / h, v = c[2] / h;
-        sx = axis_speed_ref(P, h, u, v);
-        sy = (A.dim == 2) ? axis_speed_ref(P, h, v, u) : 0.0;
+        sx = axis_speed_ref<SH>(P, h, u, v);
+        sy = (A.dim == 2) ? axis_speed_ref<SH>(P, h, v, u) : 0.0;
     } else {
         const double rh = rcp(h);
         const double u = c[1] * rh, v = c[2] * rh;
         const double gh = P.g * h;
         const double s2 = fma(u, u, v * v);
         double dqx = 0, dqy = 0, om;
-        grass_terms_fast(P, u, v, s2, om, dqx);
+        ShieldsRates LR;
+        if constexpr (SH) {
+            LR = shields_rates_fast(P, h, s2);
+            shields_terms_fast(LR, u, s2, om, dqx);
+        } else {
+            grass_terms_fast(P, u, v, s2, om, dqx);
+        }
         const double au = fabs(u), av = fabs(v);
         sx = au + fsqrt(smax(gh, fma(u, u, P.g * dqx)));
         if (A.dim == 2) {
-            grass_terms_fast(P, v, u, s2, om, dqy);
+            if constexpr (SH)
+                shields_terms_fast(LR, v, s2, om, dqy);
+            else
+                grass_terms_fast(P, v, u, s2, om, dqy);
             sy = av + fsqrt(smax(gh, fma(v, v, P.g * dqy)));
         } else {
             sy = 0.0;
@@ -325,16 +334,16 @@ __device__ __forceinline__ void reduce_flush(Reduce R, Slot& s) {
     }
 }
 
-template <bool S>
+template <bool S, bool SH>
 __device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4], Side& sx, Side& sy,
                                            bool need_x) {
     if constexpr (S) {
-        if (need_x) sx = make_side_ref(A.P, c[0], c[1], c[2], c[3]);
-        sy = make_side_ref(A.P, c[0], c[2], c[1], c[3]);
+        if (need_x) sx = make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3]);
+        sy = make_side_ref<SH>(A.P, c[0], c[2], c[1], c[3]);
     } else {
-        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
-        if (need_x) sx = make_side_fast(A.P, pre, true);
-        sy = make_side_fast(A.P, pre, false);
+        const CellPre pre = cell_pre_fast<SH>(A.P, c[0], c[1], c[2], c[3]);
+        if (need_x) sx = make_side_fast<SH>(A.P, pre, true);
+        sy = make_side_fast<SH>(A.P, pre, false);
     }
 }
 
@@ -474,26 +483,26 @@ __device__ __forceinline__ Side side_from_ring(const double (*ring)[W], int lane
     return s;
 }
 
-template <bool S>
+template <bool S, bool SH>
 __device__ __forceinline__ Side side_of(const StepArgs& A, const double c[4], bool xaxis) {
     if constexpr (S) {
-        return xaxis ? make_side_ref(A.P, c[0], c[1], c[2], c[3])
-                     : make_side_ref(A.P, c[0], c[2], c[1], c[3]);
+        return xaxis ? make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3])
+                     : make_side_ref<SH>(A.P, c[0], c[2], c[1], c[3]);
     } else {
-        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
-        return make_side_fast(A.P, pre, xaxis);
+        const CellPre pre = cell_pre_fast<SH>(A.P, c[0], c[1], c[2], c[3]);
+        return make_side_fast<SH>(A.P, pre, xaxis);
     }
 }
 
-template <bool S>
+template <bool S, bool SH>
 __device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], Side& sx, Side& sy) {
     if constexpr (S) {
-        sx = make_side_ref(A.P, c[0], c[1], c[2], c[3]);
-        sy = make_side_ref(A.P, c[0], c[2], c[1], c[3]);
+        sx = make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3]);
+        sy = make_side_ref<SH>(A.P, c[0], c[2], c[1], c[3]);
     } else {
-        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
-        sx = make_side_fast(A.P, pre, true);
-        sy = make_side_fast(A.P, pre, false);
+        const CellPre pre = cell_pre_fast<SH>(A.P, c[0], c[1], c[2], c[3]);
+        sx = make_side_fast<SH>(A.P, pre, true);
+        sy = make_side_fast<SH>(A.P, pre, false);
     }
 }
 
@@ -508,7 +517,7 @@ struct StepSmem {
     long long cprev[4][kStepThreads];     // previous row (bits), quiescence test
 };
 
-template <bool S>
+template <bool S, bool SH>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
     // Per-thread march state in shared memory (SoA by thread: conflict-free),
     // so that registers at each face solve hold little beyond the solver.
@@ -622,7 +631,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                         out3[off] = c[3];
                         if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, c);
                         if (!qvalid) {  // first row of the streak: its speeds, folded once
-                            cell_speeds<S>(A, c, qsx, qsy);
+                            cell_speeds<S, SH>(A, c, qsx, qsy);
                             reduce_fold(A, R, c, qsx, qsy);
                             qvalid = true;
                         }
@@ -637,7 +646,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         Flux fy{0, 0, 0, 0, 0};
         {
             Side sx, sy;
-            sides_of<S>(A, c, sx, sy);
+            sides_of<S, SH>(A, c, sx, sy);
             if (own_row) side_to_ring(sh_sx, sx, t);
             if (r > jb - 1 && owned) {
                 const Side lo = side_from_ring(sh_side, t);
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             out3[off] = o[3];
             if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, o);
             double ssx, ssy;
-            cell_speeds<S>(A, o, ssx, ssy);
+            cell_speeds<S, SH>(A, o, ssx, ssy);
             reduce_fold(A, R, o, ssx, ssy);
         }
         if (!own_row) continue;  // warp-uniform
@@ -695,7 +704,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
 }
 
 // ---- K2: 1D step (step_1d, src/stepper.cpp:118-140) ----------------------
-template <bool S>
+template <bool S, bool SH>
 __global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li) {
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
@@ -716,10 +725,10 @@ __global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li
     load_cell(A, p, col, 0, c);
     Side sx;
     if constexpr (S) {
-        sx = make_side_ref(A.P, c[0], c[1], c[2], c[3]);
+        sx = make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3]);
     } else {
-        const CellPre pre = cell_pre_fast(A.P, c[0], c[1], c[2], c[3]);
-        sx = make_side_fast(A.P, pre, true);
+        const CellPre pre = cell_pre_fast<SH>(A.P, c[0], c[1], c[2], c[3]);
+        sx = make_side_fast<SH>(A.P, pre, true);
     }
     const Side right = shfl_down_side(sx);
     Flux fx{0, 0, 0, 0, 0};
@@ -740,14 +749,14 @@ __global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li
 #pragma unroll
         for (int f = 0; f < 4; ++f) A.state[q][f][col] = o[f];
         double ssx, ssy;
-        cell_speeds<S>(A, o, ssx, ssy);
+        cell_speeds<S, SH>(A, o, ssx, ssy);
         reduce_fold(A, R, o, ssx, ssy);
     }
     reduce_flush(R, nxt);
 }
 
 // ---- initial reduction of a state (first cfl_dt + hmax + ghost rows) --------
-template <bool S>
+template <bool S, bool SH>
 __global__ void __launch_bounds__(256) reduce_state_kernel(StepArgs A, int li) {
     Slot& s = A.ctl->slot[li % 3];
     const int p = (int)(s.steps & 1);
@@ -760,14 +769,14 @@ __global__ void __launch_bounds__(256) reduce_state_kernel(StepArgs A, int li) {
         load_interior(A, p, col, row, c);
         if (A.write_edges_in_reduce) write_edges(A, p, col, row, c);
         double sx = 0, sy = 0;
-        if (c[0] > A.P.h_dry) cell_speeds<S>(A, c, sx, sy);
+        if (c[0] > A.P.h_dry) cell_speeds<S, SH>(A, c, sx, sy);
         reduce_fold(A, R, c, sx, sy);
     }
     reduce_flush(R, s);
 }
 
 // ---- batch of interface problems (unit tests / ABI silt_riemann_batch) -------
-template <bool S>
+template <bool S, bool SH>
 __global__ void face_batch_kernel(Params P, const double* L, const double* Rr, long long n,
                                   int axis, double* out, unsigned* err) {
     const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -780,13 +789,13 @@ __global__ void face_batch_kernel(Params P, const double* L, const double* Rr, l
     Side sl, sr;
     const int nn = axis == 0 ? 1 : 2, tt = axis == 0 ? 2 : 1;
     if constexpr (S) {
-        sl = make_side_ref(P, l[0], l[nn], l[tt], l[3]);
-        sr = make_side_ref(P, r[0], r[nn], r[tt], r[3]);
+        sl = make_side_ref<SH>(P, l[0], l[nn], l[tt], l[3]);
+        sr = make_side_ref<SH>(P, r[0], r[nn], r[tt], r[3]);
     } else {
-        const CellPre pl = cell_pre_fast(P, l[0], l[1], l[2], l[3]);
-        const CellPre pr = cell_pre_fast(P, r[0], r[1], r[2], r[3]);
-        sl = make_side_fast(P, pl, axis == 0);
-        sr = make_side_fast(P, pr, axis == 0);
+        const CellPre pl = cell_pre_fast<SH>(P, l[0], l[1], l[2], l[3]);
+        const CellPre pr = cell_pre_fast<SH>(P, r[0], r[1], r[2], r[3]);
+        sl = make_side_fast<SH>(P, pl, axis == 0);
+        sr = make_side_fast<SH>(P, pr, axis == 0);
     }
     Flux F;
     if (!face_flux<S>(P, sl, sr, F)) atomicOr(err, kErrRiemann);
@@ -797,31 +806,76 @@ __global__ void face_batch_kernel(Params P, const double* L, const double* Rr, l
     out[5 * k + 4] = F.z;
 }
 
+// ---- batch of law evaluations (unit tests / ABI silt_law_batch) -------------
+// Each variant evaluates the law the way its step kernels do: STRICT through
+// normal_flux_ref / normal_flux_derivative_ref, FAST through the per-cell
+// rates + planar terms of make_side_fast.
+template <bool S, bool SH>
+__global__ void law_batch_kernel(Params P, const double* X, long long n, double* out) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double h = X[3 * k], un = X[3 * k + 1], ut = X[3 * k + 2];
+    double omega, dq;
+    if constexpr (S) {
+        omega = normal_flux_ref<SH>(P, h, un, ut);
+        dq = normal_flux_derivative_ref<SH>(P, h, un, ut);
+    } else {
+        const double s2 = fma(un, un, ut * ut);
+        if constexpr (SH)
+            shields_terms_fast(shields_rates_fast(P, h, s2), un, s2, omega, dq);
+        else
+            grass_terms_fast(P, un, ut, s2, omega, dq);
+    }
+    out[2 * k] = omega;
+    out[2 * k + 1] = dq;
+}
+
 }  // namespace silt_dev
 
-// Explicit instantiation hooks, defined by each TU with its own S.
+// Explicit instantiation hooks, defined by each TU with its own S; the law
+// kind (A.P.shields) picks the kernel instantiation at launch.
 #define SILT_DEFINE_LAUNCHERS(S, NAME)                                                          \
-    void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st) {                    \
+    template <bool SH>                                                                           \
+    static void NAME##_step_t(const StepArgs& A, int li, dim3 grid, cudaStream_t st) {           \
         if (A.dim == 2) {                                                                        \
             static bool attr_set = false;                                                        \
             if (!attr_set) {                                                                     \
-                cudaFuncSetAttribute(silt_dev::step2d_kernel<S>,                                 \
+                cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH>,                             \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,                \
                                      (int)sizeof(silt_dev::StepSmem));                           \
                 attr_set = true;                                                                 \
             }                                                                                    \
-            silt_dev::step2d_kernel<S>                                                           \
+            silt_dev::step2d_kernel<S, SH>                                                       \
                 <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);                 \
         } else                                                                                   \
-            silt_dev::step1d_kernel<S><<<grid, kStepThreads, 0, st>>>(A, li);                    \
+            silt_dev::step1d_kernel<S, SH><<<grid, kStepThreads, 0, st>>>(A, li);                \
+    }                                                                                            \
+    void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st) {                    \
+        if (A.P.shields)                                                                         \
+            NAME##_step_t<true>(A, li, grid, st);                                                \
+        else                                                                                     \
+            NAME##_step_t<false>(A, li, grid, st);                                               \
     }                                                                                            \
     void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st) {                 \
-        silt_dev::reduce_state_kernel<S><<<blocks, 256, 0, st>>>(A, li);                         \
+        if (A.P.shields)                                                                         \
+            silt_dev::reduce_state_kernel<S, true><<<blocks, 256, 0, st>>>(A, li);               \
+        else                                                                                     \
+            silt_dev::reduce_state_kernel<S, false><<<blocks, 256, 0, st>>>(A, li);              \
     }                                                                                            \
     void NAME##_faces(const silt_dev::Params& P, const double* L, const double* R, long long n,  \
                       int axis, double* out, unsigned* err, cudaStream_t st) {                   \
         const int b = 128;                                                                       \
-        silt_dev::face_batch_kernel<S><<<(unsigned)((n + b - 1) / b), b, 0, st>>>(P, L, R, n,    \
-                                                                                  axis, out,     \
-                                                                                  err);          \
+        const unsigned g = (unsigned)((n + b - 1) / b);                                          \
+        if (P.shields)                                                                           \
+            silt_dev::face_batch_kernel<S, true><<<g, b, 0, st>>>(P, L, R, n, axis, out, err);   \
+        else                                                                                     \
+            silt_dev::face_batch_kernel<S, false><<<g, b, 0, st>>>(P, L, R, n, axis, out, err);  \
+    }                                                                                            \
+    void NAME##_law(const silt_dev::Params& P, const double* X, long long n, double* out,        \
+                    cudaStream_t st) {                                                           \
+        const unsigned g = (unsigned)((n + 127) / 128);                                          \
+        if (P.shields)                                                                           \
+            silt_dev::law_batch_kernel<S, true><<<g, 128, 0, st>>>(P, X, n, out);                \
+        else                                                                                     \
+            silt_dev::law_batch_kernel<S, false><<<g, 128, 0, st>>>(P, X, n, out);               \
     }

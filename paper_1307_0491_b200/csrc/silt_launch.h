@@ -8,7 +8,9 @@
     void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st);                 \
     void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st);              \
     void NAME##_faces(const silt_dev::Params& P, const double* L, const double* R,           \
-                      long long n, int axis, double* out, unsigned* err, cudaStream_t st);
+                      long long n, int axis, double* out, unsigned* err, cudaStream_t st);   \
+    void NAME##_law(const silt_dev::Params& P, const double* X, long long n, double* out,    \
+                    cudaStream_t st);
 
 SILT_DECLARE_LAUNCHERS(silt_fast)
 SILT_DECLARE_LAUNCHERS(silt_strict)

@@ -140,26 +140,124 @@ __device__ __forceinline__ double grass_flux(double u, double a_g, double m_g) {
     return a_g * u * abs_pow(fabs(u), m_g - 1.0);
 }
 
-// normal_flux: src/bedload.cpp:207-213 (STRICT)
-__device__ __forceinline__ double normal_flux_ref(const Params& P, double un, double ut) {
-    const double speed = hypot_glibc(un, ut);
-    if (speed <= kUEps) return 0.0;
-    return grass_flux(speed, P.a_g, P.m_g) * (un / speed);
+// ---- Shields-threshold closures (STRICT: the reference's expressions) ----
+// The template flag SH selects the law kind at compile time (one kernel
+// instantiation per kind), so the Grass instantiation carries none of this.
+
+__device__ __forceinline__ double positive_part(double x) { return x > 0 ? x : 0.0; }
+
+// friction_slope: src/bedload.cpp:82-92
+__device__ __forceinline__ double friction_slope_ref(const Params& P, double u, double h) {
+    if (!(h > 0)) return 0.0;
+    const double drag = u * fabs(u);
+    if (P.friction == 0) return P.fcoef * drag / (8.0 * P.g * h);
+    return P.fcoef * P.fcoef * drag / pow(h, 4.0 / 3.0);
 }
 
-// normal_flux_derivative: src/bedload.cpp:215-223 (STRICT); flux_derivatives
-// Grass branch :165-177 inlined.
+// shields_flux: src/bedload.cpp:94-116
+__device__ __forceinline__ double shields_flux_ref(int formula, double tau, double tau_cr) {
+    switch (formula) {
+        case 0: {
+            const double e = positive_part(tau - tau_cr);
+            return 8.0 * e * sqrt(e);
+        }
+        case 1: {
+            const double e = positive_part(tau - tau_cr);
+            return 5.7 * e * sqrt(e);
+        }
+        case 2:
+            if (tau <= 0) return 0.0;
+            return 12.0 * sqrt(tau) * positive_part(tau - tau_cr);
+        case 3:
+            return 11.0 * pow(positive_part(tau - tau_cr), 1.65);
+        default:
+            if (tau <= 0) return 0.0;
+            return 12.0 * tau * sqrt(tau) * exp(-4.5 * tau_cr / tau);
+    }
+}
+
+// shields_flux_derivative: src/bedload.cpp:118-147 (upper one-sided at the kink)
+__device__ __forceinline__ double shields_dflux_ref(int formula, double tau, double tau_cr) {
+    switch (formula) {
+        case 0:
+            if (tau < tau_cr) return 0.0;
+            return 12.0 * sqrt(tau - tau_cr);
+        case 1:
+            if (tau < tau_cr) return 0.0;
+            return 8.55 * sqrt(tau - tau_cr);
+        case 2: {
+            if (tau <= 0 || tau < tau_cr) return 0.0;
+            const double rt = sqrt(tau);
+            return 6.0 * (tau - tau_cr) / rt + 12.0 * rt;
+        }
+        case 3:
+            if (tau < tau_cr) return 0.0;
+            return 11.0 * 1.65 * pow(positive_part(tau - tau_cr), 0.65);
+        default: {
+            if (tau <= 0) return 0.0;
+            const double rt = sqrt(tau);
+            return 12.0 * exp(-4.5 * tau_cr / tau) * (1.5 * rt + 4.5 * tau_cr / rt);
+        }
+    }
+}
+
+// shields_stress: src/bedload.cpp:149-153
+__device__ __forceinline__ double shields_stress_ref(const Params& P, double h, double u) {
+    if (!(h > 0)) return 0.0;
+    const double sf = friction_slope_ref(P, fabs(u), h);
+    return h * sf / ((P.rel_density - 1.0) * P.d_s);
+}
+
+// dimensional_flux: src/bedload.cpp:155-163.  P.scale is
+// sqrt((s - 1) * g * d * d * d) evaluated on the host in the same order.
+template <bool SH>
+__device__ __forceinline__ double dimensional_flux_ref(const Params& P, double h, double u) {
+    if constexpr (!SH) {
+        return grass_flux(u, P.a_g, P.m_g);
+    } else {
+        if (!(h > 0) || fabs(u) <= kUEps) return 0.0;
+        const double tau = shields_stress_ref(P, h, u);
+        const double qstar = shields_flux_ref(P.formula, tau, P.tau_cr);
+        return copysign(qstar * P.scale, u);
+    }
+}
+
+// flux_derivatives(...).dqs_du: src/bedload.cpp:165-200 (only dqs_du feeds
+// the path, through normal_flux_derivative).
+template <bool SH>
+__device__ __forceinline__ double dqs_du_ref(const Params& P, double h, double hu) {
+    if (!(h > 0)) return 0.0;
+    const double u = hu / h;
+    if constexpr (!SH) {
+        return P.a_g * P.m_g * abs_pow(fabs(u), P.m_g - 1.0);
+    } else {
+        if (fabs(u) <= kUEps) return 0.0;
+        const double tau = shields_stress_ref(P, h, u);
+        const double dqstar = shields_dflux_ref(P.formula, tau, P.tau_cr);
+        if (dqstar == 0.0) return 0.0;
+        const double dtau_du = 2.0 * tau / u;
+        const double sgn = (u > 0) ? 1.0 : -1.0;
+        return sgn * P.scale * dqstar * dtau_du;
+    }
+}
+
+// normal_flux: src/bedload.cpp:207-213 (STRICT)
+template <bool SH>
+__device__ __forceinline__ double normal_flux_ref(const Params& P, double h, double un,
+                                                  double ut) {
+    const double speed = hypot_glibc(un, ut);
+    if (speed <= kUEps) return 0.0;
+    return dimensional_flux_ref<SH>(P, h, speed) * (un / speed);
+}
+
+// normal_flux_derivative: src/bedload.cpp:215-223 (STRICT)
+template <bool SH>
 __device__ __forceinline__ double normal_flux_derivative_ref(const Params& P, double h,
                                                              double un, double ut) {
     const double speed = hypot_glibc(un, ut);
     if (speed <= kUEps) return 0.0;
-    const double rate = grass_flux(speed, P.a_g, P.m_g);
-    double drate = 0.0;
-    const double hu = h * speed;
-    if (h > 0) {
-        const double u = hu / h;
-        drate = P.a_g * P.m_g * abs_pow(fabs(u), P.m_g - 1.0);
-    }
+    const double rate = dimensional_flux_ref<SH>(P, h, speed);
+    const double drate = dqs_du_ref<SH>(P, h, h * speed);
     const double ratio = un / speed;
     return rate / speed + ratio * ratio * (drate - rate / speed);
 }
@@ -188,6 +286,78 @@ __device__ __forceinline__ void grass_terms_fast(const Params& P, double un, dou
     dq = rate * is + ratio * ratio * (drate - rate * is);
 }
 
+// Shields rate / speed and d rate / d speed at speed s = sqrt(s2) (FAST):
+// tau = ktau s^2 (Darcy-Weisbach, depth-free) or ktau s^2 h^(-1/3) (Manning),
+// q* and dq*/dtau share their sqrt / pow / exp, dtau/ds = 2 tau / s.
+struct ShieldsRates {
+    double rs, dr;  // rate / s, d rate / d s  (both 0 when transport-free)
+};
+
+__device__ __forceinline__ ShieldsRates shields_rates_fast(const Params& P, double h, double s2) {
+    ShieldsRates R{0.0, 0.0};
+    if (!(s2 > kUEps * kUEps) || !(h > 0)) return R;
+    double tau = P.ktau * s2;
+    if (P.friction != 0) tau *= rcbrt(h);
+    const double tc = P.tau_cr;
+    const double e = positive_part(tau - tc);
+    const bool above = tau >= tc;  // upper one-sided derivative at the kink
+    double q, dqs;
+    switch (P.formula) {
+        case 0: case 1: {
+            const double re = fsqrt(e);
+            const double c = P.formula == 0 ? 8.0 : 5.7;
+            q = c * e * re;
+            dqs = above ? 1.5 * c * re : 0.0;
+            break;
+        }
+        case 2: {
+            if (!(tau > 0)) return R;
+            const double rt = fsqrt(tau);
+            q = 12.0 * rt * e;
+            dqs = above ? fma(6.0 * e, rcp(rt), 12.0 * rt) : 0.0;
+            break;
+        }
+        case 3: {
+            const double p = pow(e, 0.65);
+            q = 11.0 * e * p;
+            dqs = above ? 18.15 * p : 0.0;
+            break;
+        }
+        default: {
+            if (!(tau > 0)) return R;
+            const double rt = fsqrt(tau);
+            const double it = rcp(tau);
+            const double ex = exp(-4.5 * tc * it);
+            q = 12.0 * tau * rt * ex;
+            dqs = 12.0 * ex * fma(1.5, rt, 4.5 * tc * rt * it);
+            break;
+        }
+    }
+    const double is = rcp(fsqrt(s2));
+    R.rs = P.scale * q * is;
+    R.dr = 2.0 * P.scale * dqs * tau * is;
+    return R;
+}
+
+// Planar terms from the rates: omega = rate u_n / s,
+// dq = rate / s + (u_n / s)^2 (drate - rate / s).
+__device__ __forceinline__ void shields_terms_fast(const ShieldsRates& R, double un, double s2,
+                                                   double& omega, double& dq) {
+    omega = R.rs * un;
+    const double r2 = s2 > 0.0 ? un * un * rcp(s2) : 0.0;
+    dq = fma(r2, R.dr - R.rs, R.rs);
+}
+
+template <bool SH>
+__device__ __forceinline__ void law_terms_fast(const Params& P, double h, double un, double ut,
+                                               double s2, double& omega, double& dq) {
+    if constexpr (SH) {
+        shields_terms_fast(shields_rates_fast(P, h, s2), un, s2, omega, dq);
+    } else {
+        grass_terms_fast(P, un, ut, s2, omega, dq);
+    }
+}
+
 // ---- one cell seen from one face axis ------------------------------------
 // RelaxState (include/silt/relax_state.hpp:14-22) plus the per-side pieces of
 // bounds_impl (src/relax_state.cpp:25-53) and of the Riemann solver that only
@@ -204,6 +374,7 @@ struct Side {
 
 // STRICT side: equilibrate (src/relax_state.cpp:8-21) with primitives
 // (src/grid.cpp:47-59), then the side terms of bounds_impl exactly as written.
+template <bool SH>
 __device__ __forceinline__ Side make_side_ref(const Params& P, double h, double hu_n,
                                               double hu_t, double zb) {
     Side s;
@@ -214,17 +385,17 @@ __device__ __forceinline__ Side make_side_ref(const Params& P, double h, double 
     s.hun = h * un_p;
     s.pi = 0.5 * P.g * h * h;
     s.z = zb;
-    s.omega = normal_flux_ref(P, un_p, ut_p);
+    s.omega = normal_flux_ref<SH>(P, h, un_p, ut_p);
     s.ut = ut_p;
     s.wet = wet;
     s.un = wet ? s.hun / h : 0.0;
     s.tau = 1.0 / smax(h, 1e-12);
     if (wet) {
         s.a_side = h * sqrt(P.g * h);
-        const double dq = normal_flux_derivative_ref(P, h, s.un, ut_p);
+        const double dq = normal_flux_derivative_ref<SH>(P, h, s.un, ut_p);
         s.b2_side = s.hun * s.hun + P.g * h * h * dq;
         const double speed = hypot_glibc(s.un, ut_p);
-        s.moving = (grass_flux(speed, P.a_g, P.m_g) != 0.0 || dq != 0.0 || s.omega != 0.0);
+        s.moving = (dimensional_flux_ref<SH>(P, h, speed) != 0.0 || dq != 0.0 || s.omega != 0.0);
     } else {
         s.a_side = 0.0;
         s.b2_side = 0.0;
@@ -237,9 +408,11 @@ __device__ __forceinline__ Side make_side_ref(const Params& P, double h, double 
 struct CellPre {
     double h, hu, hv, zb;
     double u, v, s2, pi, tau, sq;  // sq = sqrt(g h)
+    ShieldsRates law;              // Shields only (dead in the Grass instantiation)
     int wet;
 };
 
+template <bool SH>
 __device__ __forceinline__ CellPre cell_pre_fast(const Params& P, double h, double hu, double hv,
                                                  double zb) {
     CellPre c;
@@ -255,10 +428,12 @@ __device__ __forceinline__ CellPre cell_pre_fast(const Params& P, double h, doub
     c.pi = P.half_g * h * h;
     c.tau = (h < 1e-12) ? (1.0 / 1e-12) : rh;  // tau_of, src/riemann.cpp:50-52
     c.sq = c.wet ? fsqrt(P.g * h) : 0.0;
+    if constexpr (SH) c.law = shields_rates_fast(P, h, c.s2);
     return c;
 }
 
 // FAST side for axis X (xaxis=1: normal u) or Y (normal v).
+template <bool SH>
 __device__ __forceinline__ Side make_side_fast(const Params& P, const CellPre& c, bool xaxis) {
     Side s;
     const double un = xaxis ? c.u : c.v;
@@ -268,7 +443,10 @@ __device__ __forceinline__ Side make_side_fast(const Params& P, const CellPre& c
     s.pi = c.pi;
     s.z = c.zb;
     double dq;
-    grass_terms_fast(P, un, ut, c.s2, s.omega, dq);
+    if constexpr (SH)
+        shields_terms_fast(c.law, un, c.s2, s.omega, dq);
+    else
+        grass_terms_fast(P, un, ut, c.s2, s.omega, dq);
     if (!c.wet) {
         s.omega = 0.0;
         dq = 0.0;
@@ -279,7 +457,10 @@ __device__ __forceinline__ Side make_side_fast(const Params& P, const CellPre& c
     s.wet = c.wet;
     s.a_side = c.wet ? c.h * c.sq : 0.0;
     s.b2_side = c.wet ? fma(s.hun, s.hun, P.g * c.h * c.h * dq) : 0.0;
-    s.moving = c.wet && P.a_g != 0.0 && c.s2 > 0.0;
+    if constexpr (SH)
+        s.moving = c.wet && (dq != 0.0 || s.omega != 0.0);
+    else
+        s.moving = c.wet && P.a_g != 0.0 && c.s2 > 0.0;
     return s;
 }
 
@@ -732,9 +913,10 @@ __device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const 
 }
 
 // axis_speed: src/stepper.cpp:30-36 (STRICT, on primitives)
+template <bool SH>
 __device__ __forceinline__ double axis_speed_ref(const Params& P, double h, double un, double ut) {
     const double fluid = fabs(un) + sqrt(P.g * h);
-    const double dq = normal_flux_derivative_ref(P, h, un, ut);
+    const double dq = normal_flux_derivative_ref<SH>(P, h, un, ut);
     const double solid = fabs(un) + sqrt(un * un + P.g * dq);
     return smax(fluid, solid);
 }

@@ -80,6 +80,7 @@ def lib() -> C.CDLL:
         "silt_cfl_dt": ([_P, _D, C.c_int, _D], C.c_int),
         "silt_step_padded": ([_P, _D, C.c_double, C.c_int], C.c_int),
         "silt_riemann_batch": ([_P, _D, _D, C.c_int64, C.c_int, C.c_int, _D], C.c_int),
+        "silt_law_batch": ([_P, _D, C.c_int64, C.c_int, _D], C.c_int),
         "silt_selftest_math": ([_D, _D, C.c_int64, _D], C.c_int),
         "silt_group_create": ([_P, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int,
                                C.POINTER(_VP)], C.c_int),
@@ -277,6 +278,16 @@ def faces(problem: SiltProblem, left: np.ndarray, right: np.ndarray, axis: int,
     out = np.empty((left.shape[0], 5))
     check(lib().silt_riemann_batch(C.byref(problem), _dp(left), _dp(right), left.shape[0],
                                    axis, variant, _dp(out)))
+    return out
+
+
+def law_terms(problem: SiltProblem, states: np.ndarray,
+              variant: int = abi.VARIANT_FAST) -> np.ndarray:
+    """(n, 2): normal_flux, normal_flux_derivative of states (n, 3) = (h, u_n, u_t)."""
+    states = np.ascontiguousarray(states, dtype=np.float64).reshape(-1, 3)
+    out = np.empty((states.shape[0], 2))
+    check(lib().silt_law_batch(C.byref(problem), _dp(states), states.shape[0], variant,
+                               _dp(out)))
     return out
 
 

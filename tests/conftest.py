@@ -72,7 +72,17 @@ def problem_from_meta(case: dict):
                          safety=case["safety"])
     for s, (t, sup, q0, h0) in enumerate(case["bc"]):
         p.bc[s] = abi.SiltBC(t, sup, q0, h0)
+    if "law" in case:  # Shields fixtures (tests/golden/make_golden_shields.py)
+        abi.set_shields(p, **case["law"])
     return p
+
+
+@pytest.fixture(scope="session")
+def golden_shields():
+    data = np.load(os.path.join(GOLDEN_DIR, "golden_shields.npz"))
+    with open(os.path.join(GOLDEN_DIR, "golden_shields.json")) as fh:
+        meta = json.load(fh)
+    return data, meta
 
 
 def normwise(a: np.ndarray, b: np.ndarray) -> np.ndarray:

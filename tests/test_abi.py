@@ -62,8 +62,8 @@ def test_validation_without_device(native):
     with pytest.raises(native.InvalidArgument, match="periodic"):
         native.Solver(p)
     p = abi.make_problem(2, 4, 4, 1.0, 1.0, a_g=0.1)
-    p.law_kind = 1
-    with pytest.raises(NotImplementedError, match="Grass"):
+    p.law_kind = 2
+    with pytest.raises(native.InvalidArgument, match="law kind"):
         native.Solver(p)
     p = abi.make_problem(2, 4, 4, 1.0, 1.0, a_g=0.1)
     bad = abi.SiltStrip(0, 9, 0, 0)
