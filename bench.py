@@ -99,7 +99,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def build_global_problem(wl: str, world: int):
+def apply_law(p, law: str):
+    """--law grass (BASELINE's workloads) or <formula>:<friction>, e.g.
+    mpm:manning — BedloadLaw::shields with the config layer's defaults."""
+    from paper_1307_0491_b200 import abi
+    if law != "grass":
+        formula, friction = law.split(":")
+        abi.set_shields(p, formula, friction)
+    return p
+
+
+def build_global_problem(wl: str, world: int, law: str = "grass"):
     from paper_1307_0491_b200 import abi
     w = WORKLOADS[wl]
     if w["kind"] in ("dune", "uniform"):
@@ -108,7 +118,7 @@ def build_global_problem(wl: str, world: int):
     else:
         ny = w["ny_per_gpu"] * world
         p = abi.make_problem(2, w["nx"], ny, 1.0, 1.0, a_g=w["a_g"], cfl=w["cfl"])
-    return p
+    return apply_law(p, law)
 
 
 def device_initial_rows(wl: str, p, j0: int, nrows: int, device):
@@ -156,7 +166,7 @@ def device_initial_rows(wl: str, p, j0: int, nrows: int, device):
     return out
 
 
-def cpu_reference_sample(wl: str, steps: int, threads: int):
+def cpu_reference_sample(wl: str, steps: int, threads: int, law: str = "grass"):
     """The reference's CPU run_parallel (oracle/_ref) on a bounded row sample
     of the workload; returns (cell-updates/s, description)."""
     import numpy as np
@@ -182,6 +192,7 @@ def cpu_reference_sample(wl: str, steps: int, threads: int):
     else:
         p, init, _ = S.random_bed_2d(w["nx"], 64, a_g=w["a_g"], cfl=w["cfl"])
         desc = f"{wl} {w['nx']} x 64 rows"
+    apply_law(p, law)
     R = O.reference() if O.have_reference() else None
     kind = "reference"
     if R is None:
@@ -207,7 +218,7 @@ def run_reference_arm(args):
     total_cells = 0.0
     total_secs = 0.0
     for s in range(args.warmup + args.steps):
-        rate, desc, kind, used = cpu_reference_sample(args.workload, 1, threads)
+        rate, desc, kind, used = cpu_reference_sample(args.workload, 1, threads, args.law)
         if s >= args.warmup:
             total_secs += 1.0 / rate
             total_cells += 1.0
@@ -216,7 +227,7 @@ def run_reference_arm(args):
         "metric": "cell-updates/s (fp64, 2D)", "value": value, "unit": "cell-updates/s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "sample": desc},
+        "config": {"workload": args.workload, "law": args.law, "sample": desc},
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": used, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
@@ -234,6 +245,10 @@ def main():
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="fast", choices=["fast", "strict"])
+    ap.add_argument("--law", default="grass",
+                    help="grass (BASELINE workloads) or <formula>:<friction>, "
+                         "formula in mpm|flvb|nielsen|ribberink|camenen, "
+                         "friction in manning|darcy-weisbach")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"],
@@ -252,7 +267,7 @@ def main():
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     variant = abi.VARIANT_FAST if args.variant == "fast" else abi.VARIANT_STRICT
-    p = build_global_problem(args.workload, world)
+    p = build_global_problem(args.workload, world, args.law)
     partition = None
     if world > 1 and args.partition == "balanced" and WORKLOADS[args.workload]["kind"] == "dune":
         # Work-balanced row strips (quiescent rows are cheaper).  Every rank
@@ -356,7 +371,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, desc, kind, used = cpu_reference_sample(args.workload, 3, os.cpu_count() or 1)
+            rate, desc, kind, used = cpu_reference_sample(args.workload, 3, os.cpu_count() or 1, args.law)
             cpu = {"value": rate, "unit": "cell-updates/s", "cores": used, "kind": kind,
                    "sample": desc}
         except Exception as e:  # noqa: BLE001
@@ -379,7 +394,7 @@ def main():
             "data": "synthetic",
             "variant": args.variant,
             "config": {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
-                       "nx": p.nx, "ny": p.ny, "rows_per_gpu": nrows,
+                       "law": args.law, "nx": p.nx, "ny": p.ny, "rows_per_gpu": nrows,
                        "parallelism": f"row strips x{world}",
                        "partition": (args.partition if world > 1 else "single strip"),
                        "l2": "state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells},
