@@ -31,6 +31,9 @@
  *                                    (src/parallel.cpp:43-99, 192-206)
  *   silt_solver_download ........... PaddedField::interior, gather
  *                                    (src/stepper.cpp:20-25, src/parallel.cpp:179-190)
+ *   silt_solver_capture_resume ..... on_snapshot(t, gather(...)) at a landed
+ *                                    snapshot time, asynchronously
+ *                                    (src/parallel.cpp:333-342)
  *   silt_run ....................... run_serial (src/parallel.cpp:208-259)
  *   silt_cfl_dt .................... cfl_dt (include/silt/stepper.hpp:38-41)
  *   silt_step_padded ............... step_1d / step_2d on a halo-complete
@@ -211,6 +214,20 @@ int silt_solver_step_fixed(silt_solver* s, double dt);
 int silt_solver_status(silt_solver* s, silt_status* st);
 /* Continue after a snapshot pause. */
 int silt_solver_resume(silt_solver* s);
+/* Asynchronous snapshot gather: the on_snapshot + gather of a run
+ * (src/parallel.cpp:333-342, 179-190) without holding the run.  For a PAUSED
+ * solver: the state is copied on the device into a snapshot buffer, the
+ * solver resumes, and the buffer streams to host_aos (nx * ny_local FlowState,
+ * AoS) on a side stream while the following steps execute.  Use page-locked
+ * host memory (silt_host_alloc) for the copy to overlap.  One capture is in
+ * flight per solver; the next capture waits for it.  capture_wait blocks until
+ * the last capture has landed; capture_query reports it without blocking. */
+int silt_solver_capture_resume(silt_solver* s, double* host_aos);
+int silt_solver_capture_wait(silt_solver* s);
+int silt_solver_capture_query(silt_solver* s, int* landed);
+/* Page-locked host memory (capture targets, fast uploads). */
+int silt_host_alloc(int64_t bytes, void** out);
+int silt_host_free(void* p);
 /* dt of steps [0, n) from the device log (n <= capacity). */
 int silt_solver_dt_log(silt_solver* s, double* host_out, int64_t n);
 /* Current cfl_dt of the uploaded state (synchronises). */
@@ -240,6 +257,9 @@ int silt_group_begin(silt_group* g, const silt_run_plan* plan);
 int silt_group_step(silt_group* g, int n);
 int silt_group_status(silt_group* g, silt_status* st);
 int silt_group_resume(silt_group* g);
+/* silt_solver_capture_resume / _wait over every strip (whole-grid host_aos) */
+int silt_group_capture_resume(silt_group* g, double* host_aos);
+int silt_group_capture_wait(silt_group* g);
 int silt_group_dt_log(silt_group* g, double* host_out, int64_t n);
 
 /* ---- one-shot conveniences (mirror the reference free functions) ---------- */

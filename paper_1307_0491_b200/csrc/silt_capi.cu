@@ -88,6 +88,10 @@ struct silt_solver {
     double* rows = nullptr;     // 8 x [4][nx]
     double* cols = nullptr;     // 2 x [4][ny]
     double* staging = nullptr;  // AoS nx*ny*4
+    double* snapbuf = nullptr;  // AoS nx*ny*4: device copy of a captured snapshot
+    cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
+    cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
+    bool cap_pending = false;
     Control* ctl = nullptr;
     Control* host_ctl = nullptr;  // pinned staging for control uploads
     double* dt_log = nullptr;
@@ -347,6 +351,13 @@ int silt_solver_destroy(silt_solver* s) {
     if (!s) return SILT_OK;
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->copy_stream) {
+        cudaStreamSynchronize(s->copy_stream);
+        cudaStreamDestroy(s->copy_stream);
+    }
+    if (s->cap_ready) cudaEventDestroy(s->cap_ready);
+    if (s->cap_done) cudaEventDestroy(s->cap_done);
+    cudaFree(s->snapbuf);
     cudaFree(s->planes);
     cudaFree(s->rows);
     cudaFree(s->cols);
@@ -427,6 +438,85 @@ int silt_solver_download(silt_solver* s, double* host_aos) {
 
 int silt_solver_download_device(silt_solver* s, double* dev_aos) {
     return download_impl(s, dev_aos, cudaMemcpyDeviceToDevice);
+}
+
+// ---- asynchronous snapshot capture ------------------------------------------
+// on_snapshot + gather (src/parallel.cpp:333-342, 179-190) without holding the
+// run: the paused state is transposed into snapbuf on the solver's stream, the
+// solver resumes, and snapbuf streams to host memory on copy_stream while the
+// next steps execute.
+
+int silt_solver_capture_wait(silt_solver* s) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    if (!s->cap_pending) return SILT_OK;
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaEventSynchronize(s->cap_done));
+    s->cap_pending = false;
+    return SILT_OK;
+}
+
+int silt_solver_capture_query(silt_solver* s, int* landed) {
+    if (!s || !landed) return fail(SILT_ERR_INVALID, "silt_solver_capture_query: null argument");
+    *landed = 1;
+    if (!s->cap_pending) return SILT_OK;
+    CUDA_TRY(cudaSetDevice(s->device));
+    const cudaError_t e = cudaEventQuery(s->cap_done);
+    if (e == cudaErrorNotReady) {
+        *landed = 0;
+        return SILT_OK;
+    }
+    if (e != cudaSuccess) return fail(SILT_ERR_CUDA, cudaGetErrorString(e));
+    s->cap_pending = false;
+    return SILT_OK;
+}
+
+int silt_solver_capture_resume(silt_solver* s, double* host_aos) {
+    if (!s || !host_aos) return fail(SILT_ERR_INVALID, "silt_solver_capture_resume: null argument");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_capture_resume: run not begun");
+    if (int rc = silt_solver_capture_wait(s)) return rc;  // snapbuf is free again
+    CUDA_TRY(cudaSetDevice(s->device));
+    const size_t bytes = 4 * (size_t)s->nx * s->ny * sizeof(double);
+    if (!s->snapbuf) {
+        CUDA_TRY(cudaMalloc(&s->snapbuf, bytes));
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->cap_ready, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->cap_done, cudaEventDisableTiming));
+    }
+    Slot sl;
+    if (int rc = read_slot(s, &sl, nullptr)) return rc;  // synchronizes the stream
+    if (sl.state != SILT_STATE_PAUSED)
+        return fail(SILT_ERR_INVALID, "silt_solver_capture_resume: solver is not paused");
+    const int p = (int)(sl.steps & 1);
+    const StepArgs& A = s->args;
+    soa_to_aos<<<grid_blocks((long long)s->nx * s->ny, 256), 256, 0, s->stream>>>(
+        s->snapbuf, A.state[p][0], A.state[p][1], A.state[p][2], A.state[p][3], s->nx, s->ny,
+        s->pitch);
+    ++s->kernel_count;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(s->cap_ready, s->stream));
+    CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->cap_ready, 0));
+    CUDA_TRY(cudaMemcpyAsync(host_aos, s->snapbuf, bytes, cudaMemcpyDeviceToHost,
+                             s->copy_stream));
+    CUDA_TRY(cudaEventRecord(s->cap_done, s->copy_stream));
+    s->cap_pending = true;
+    // resume: later launches on s->stream are ordered after the transpose
+    int st = SILT_STATE_RUNNING;
+    Slot* slot = &s->ctl->slot[s->launches % 3];
+    CUDA_TRY(cudaMemcpy(&slot->state, &st, sizeof(int), cudaMemcpyHostToDevice));
+    return SILT_OK;
+}
+
+int silt_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return fail(SILT_ERR_INVALID, "silt_host_alloc: bad argument");
+    *out = nullptr;
+    if (bytes == 0) return SILT_OK;
+    CUDA_TRY(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+    return SILT_OK;
+}
+
+int silt_host_free(void* p) {
+    if (p) CUDA_TRY(cudaFreeHost(p));
+    return SILT_OK;
 }
 
 int silt_solver_set_ghosts(silt_solver* s, const double* west, const double* east,
@@ -837,6 +927,21 @@ int silt_group_resume(silt_group* g) {
     if (!g) return fail(SILT_ERR_INVALID, "null group");
     for (silt_solver* s : g->strips)
         if (int rc = silt_solver_resume(s)) return rc;
+    return SILT_OK;
+}
+
+int silt_group_capture_resume(silt_group* g, double* host_aos) {
+    if (!g || !host_aos) return fail(SILT_ERR_INVALID, "silt_group_capture_resume: null argument");
+    for (silt_solver* s : g->strips)
+        if (int rc = silt_solver_capture_resume(s, host_aos + 4 * (size_t)s->strip.j0 * g->nx))
+            return rc;
+    return SILT_OK;
+}
+
+int silt_group_capture_wait(silt_group* g) {
+    if (!g) return fail(SILT_ERR_INVALID, "null group");
+    for (silt_solver* s : g->strips)
+        if (int rc = silt_solver_capture_wait(s)) return rc;
     return SILT_OK;
 }
 

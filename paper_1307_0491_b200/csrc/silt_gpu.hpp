@@ -25,6 +25,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -142,6 +143,21 @@ class Group {
     silt_group* g_ = nullptr;
 };
 
+// page-locked host memory for asynchronous snapshot captures
+struct PinnedBuffer {
+    double* ptr = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t n) {
+        void* p = nullptr;
+        check(silt_host_alloc(static_cast<int64_t>(n), &p));
+        ptr = static_cast<double*>(p);
+        bytes = n;
+    }
+    ~PinnedBuffer() {
+        if (ptr) silt_host_free(ptr);
+    }
+};
+
 // make_plan + the run loop of run_serial / run_parallel
 // (src/parallel.cpp:101-132, 208-259, 261-386)
 inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
@@ -155,6 +171,7 @@ inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
     bool snap_initial = false;
     for (double s : opt.snapshot_times)
         if (s == 0) snap_initial = true;
+    PinnedBuffer pinned;  // declared before the group: outlives any in-flight copy
     Group g(p, py);
     check(silt_group_upload(g.get(), data(sc.initial.cells)));
     if (snap_initial && opt.on_snapshot) opt.on_snapshot(0.0, sc.initial);
@@ -163,20 +180,35 @@ inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
     check(silt_group_begin(g.get(), &plan));
     const auto loop0 = std::chrono::steady_clock::now();
     silt_status st{};
+    // Snapshots are gathered asynchronously: the paused state is captured on
+    // the device, the run resumes, and the copy streams into page-locked host
+    // memory while the next steps execute; on_snapshot runs once it landed.
     Field snap(sc.grid);
+    double pending_t = -1;
+    auto deliver = [&] {
+        if (pending_t < 0) return;
+        check(silt_group_capture_wait(g.get()));
+        std::memcpy(data(snap.cells), pinned.ptr, pinned.bytes);
+        opt.on_snapshot(pending_t, snap);
+        pending_t = -1;
+    };
     for (;;) {
         check(silt_group_step(g.get(), 16));
         check(silt_group_status(g.get(), &st));
         if (st.state == SILT_STATE_PAUSED) {
             if (opt.on_snapshot) {
-                check(silt_group_download(g.get(), data(snap.cells)));
-                opt.on_snapshot(st.t, snap);
+                deliver();
+                if (!pinned.ptr) pinned.alloc(snap.cells.size() * sizeof(FlowState));
+                check(silt_group_capture_resume(g.get(), pinned.ptr));
+                pending_t = st.t;
+            } else {
+                check(silt_group_resume(g.get()));
             }
-            check(silt_group_resume(g.get()));
             continue;
         }
         if (st.state == SILT_STATE_DONE) break;
     }
+    deliver();
     const double loop_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - loop0).count();
     RunResult res;

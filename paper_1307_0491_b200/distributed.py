@@ -401,17 +401,19 @@ class LocalStripGroup:
         self.N.check(self.L.silt_group_download(self.h, self.N._dp(out)))
         return out
 
-    def run(self, batch: int = 8, on_snapshot=None):
-        while True:
-            self.step(batch)
-            st = self.status()
-            if st.state == abi.STATE_PAUSED:
-                if on_snapshot is not None:
-                    on_snapshot(st.t, self.gather())
-                self.resume()
-                continue
-            if st.state == abi.STATE_DONE:
-                return st
+    def capture_resume(self, out: np.ndarray):
+        """Asynchronous whole-grid snapshot of a paused run (every strip streams
+        its rows into ``out`` while the next steps run)."""
+        assert out.flags.c_contiguous and out.size == 4 * self.nx * self.ny
+        self.N.check(self.L.silt_group_capture_resume(self.h, self.N._dp(out)))
+
+    def capture_wait(self):
+        self.N.check(self.L.silt_group_capture_wait(self.h))
+
+    def run(self, batch: int = 8, on_snapshot=None, async_snapshots: bool = False):
+        return self.N._run_loop(self.step, self.status, self.resume, self.gather,
+                                self.capture_resume, self.capture_wait, batch, on_snapshot,
+                                async_snapshots, (self.ny, self.nx))
 
     def close(self):
         if self.h:

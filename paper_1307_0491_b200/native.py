@@ -92,6 +92,13 @@ def lib() -> C.CDLL:
         "silt_group_status": ([_VP, C.POINTER(SiltStatus)], C.c_int),
         "silt_group_resume": ([_VP], C.c_int),
         "silt_group_dt_log": ([_VP, _D, C.c_int64], C.c_int),
+        "silt_group_capture_resume": ([_VP, _D], C.c_int),
+        "silt_group_capture_wait": ([_VP], C.c_int),
+        "silt_solver_capture_resume": ([_VP, _D], C.c_int),
+        "silt_solver_capture_wait": ([_VP], C.c_int),
+        "silt_solver_capture_query": ([_VP, C.POINTER(C.c_int)], C.c_int),
+        "silt_host_alloc": ([C.c_int64, C.POINTER(_VP)], C.c_int),
+        "silt_host_free": ([_VP], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -125,6 +132,75 @@ def _plan(t_end: float, max_steps: int, snapshots, dt_cap: int):
     plan = SiltRunPlan(float(t_end), int(max_steps),
                        _dp(snaps) if snaps.size else None, int(snaps.size), int(dt_cap))
     return plan, snaps
+
+
+class PinnedField:
+    """Page-locked host field (silt_host_alloc) viewed as a (ny, nx, 4) array."""
+
+    def __init__(self, ny: int, nx: int):
+        self.L = lib()
+        self.ptr = _VP()
+        n = ny * nx * 4
+        check(self.L.silt_host_alloc(n * 8, C.byref(self.ptr)))
+        self.array = np.ctypeslib.as_array((C.c_double * n).from_address(self.ptr.value))
+        self.array = self.array.reshape(ny, nx, 4)
+
+    def close(self):
+        if self.ptr:
+            self.array = None
+            self.L.silt_host_free(self.ptr)
+            self.ptr = _VP()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _run_loop(step, status, resume, download, capture, wait, batch, on_snapshot,
+              async_snapshots, shape):
+    """The run loop shared by Solver and LocalStripGroup (src/parallel.cpp:208-259).
+
+    Synchronous snapshots: download, call on_snapshot(t, field), resume.
+    Asynchronous snapshots (``async_snapshots=True``): capture into a pinned
+    buffer and resume at once; on_snapshot(t, view) runs when the copy has
+    landed (at the latest before the next capture and at the end), while the
+    device keeps stepping.  The view is valid during the callback only, like
+    the reference's ``const Field&``.
+    """
+    pinned = None
+    pending = None
+    try:
+        while True:
+            step(batch)
+            st = status()
+            if st.state == abi.STATE_PAUSED:
+                if on_snapshot is None:
+                    resume()
+                elif not async_snapshots:
+                    on_snapshot(st.t, download())
+                    resume()
+                else:
+                    if pending is not None:
+                        wait()
+                        on_snapshot(pending, pinned.array)
+                    if pinned is None:
+                        pinned = PinnedField(*shape)
+                    capture(pinned.array)
+                    pending = st.t
+                continue
+            if st.state == abi.STATE_DONE:
+                if pending is not None:
+                    wait()
+                    on_snapshot(pending, pinned.array)
+                return st
+    finally:
+        if pinned is not None:
+            try:
+                wait()  # no copy may still target the buffer when it is freed
+            finally:
+                pinned.close()
 
 
 class Solver:
@@ -226,18 +302,20 @@ class Solver:
         check(self.L.silt_solver_launch_count(self.h, C.byref(n)))
         return n.value
 
-    def run(self, batch: int = 32, on_snapshot=None) -> SiltStatus:
+    def capture_resume(self, out: np.ndarray):
+        """Asynchronous snapshot of a paused run into ``out`` (pinned memory
+        overlaps the copy with the next steps); see silt_solver_capture_resume."""
+        assert out.flags.c_contiguous and out.size == 4 * self.nx * self.ny
+        check(self.L.silt_solver_capture_resume(self.h, _dp(out)))
+
+    def capture_wait(self):
+        check(self.L.silt_solver_capture_wait(self.h))
+
+    def run(self, batch: int = 32, on_snapshot=None, async_snapshots: bool = False) -> SiltStatus:
         """Advance until DONE; PAUSED snapshots call on_snapshot(t, field)."""
-        while True:
-            self.step(batch)
-            st = self.status()
-            if st.state == abi.STATE_PAUSED:
-                if on_snapshot is not None:
-                    on_snapshot(st.t, self.download())
-                self.resume()
-                continue
-            if st.state == abi.STATE_DONE:
-                return st
+        return _run_loop(self.step, self.status, self.resume, self.download,
+                         self.capture_resume, self.capture_wait, batch, on_snapshot,
+                         async_snapshots, (self.ny, self.nx))
 
 
 # ---- one-shot conveniences (mirror the reference free functions) -------------

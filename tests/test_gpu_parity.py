@@ -172,6 +172,47 @@ def test_snapshots_pause_and_land(N, golden):
     s.close()
 
 
+@pytest.mark.parametrize("py", [0, 1, 3])
+def test_async_snapshots(N, golden, restatement, py):
+    """Asynchronous snapshot gather (silt_solver/group_capture_resume): the run
+    resumes at once and each snapshot streams to pinned host memory while the
+    next steps execute.  Snapshots closer than one batch apart exercise a
+    capture still in flight when the next pause arrives.  STRICT: every
+    snapshot equals the reference path run to that time, bit for bit; the
+    final state equals the synchronous run's.  py = 0: single Solver; py >= 1:
+    the strip group."""
+    from paper_1307_0491_b200.distributed import LocalStripGroup
+    data, meta = golden
+    case = "rand48x32"
+    m = meta["cases"][case]
+    p = problem_from_meta(m)
+    init = data[f"{case}_init"]
+    T = m["t_final"]
+    snaps = [0.1 * T, 0.1 * T + 1e-9, 0.25 * T, 0.26 * T, 0.5 * T, 0.9 * T]
+    runs = {}
+    for mode in (False, True):
+        if py == 0:
+            h = N.Solver(p, variant=abi.VARIANT_STRICT)
+            h.upload(init)
+        else:
+            h = LocalStripGroup(p, py, devices=(0,), variant=abi.VARIANT_STRICT)
+            h.upload(init)
+        h.begin(max_steps=m["max_steps"] + len(snaps), snapshots=snaps)
+        seen = []
+        st = h.run(batch=5, on_snapshot=lambda t, f: seen.append((t, f.copy())),
+                   async_snapshots=mode)
+        final = h.download() if py == 0 else h.gather()
+        h.close()
+        runs[mode] = (seen, final, st.steps, st.t)
+    assert [t for t, _ in runs[True][0]] == snaps
+    assert runs[True][2:] == runs[False][2:]
+    assert np.array_equal(runs[True][1], runs[False][1])
+    for (t, f), (t2, f2) in zip(runs[True][0], runs[False][0]):
+        assert t == t2 and np.array_equal(f, f2)
+        ref, rt, _, _ = restatement.run(p, init, t_end=t, snapshots=[s for s in snaps if s < t])
+        assert rt == t and np.array_equal(f, ref)
+
+
 def test_dry_field_raises(N):
     p = abi.make_problem(2, 8, 8, 1.0, 1.0, a_g=0.1)
     with pytest.raises(N.InvalidArgument, match="dry"):
