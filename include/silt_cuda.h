@@ -41,6 +41,8 @@
  *   silt_riemann_batch ............. equilibrate + celerity_bounds +
  *                                    interface_riemann (relax_state.hpp:27-51,
  *                                    riemann.hpp:33-35)
+ *   silt_write_snapshot / _to_string write_snapshot / snapshot_to_string
+ *                                    (src/snapshot.cpp:50-93), on the device
  *   silt_law_batch ................. normal_flux + normal_flux_derivative
  *                                    (include/silt/bedload.hpp:95-98)
  */
@@ -261,6 +263,27 @@ int silt_group_resume(silt_group* g);
 int silt_group_capture_resume(silt_group* g, double* host_aos);
 int silt_group_capture_wait(silt_group* g);
 int silt_group_dt_log(silt_group* g, double* host_out, int64_t n);
+
+/* ---- snapshot CSV, formatted on the device -------------------------------
+ * write_snapshot / snapshot_to_string (src/snapshot.cpp:50-93; io.hpp:66-73):
+ * header `x,h,u,zb,eta,time` (1D) or `x,y,h,u,v,zb,eta,time` (2D), one row
+ * per cell, row-major, every number as snprintf("%.17g") prints it — the
+ * bytes are identical to the reference's.  Rows are formatted by GPU kernels
+ * (silt_csv.cu) in chunks and streamed through pinned memory to the sink.
+ * `aos`: rows [j0, j0 + rows) of the problem's grid as FlowState AoS, in
+ * host or device memory.  `append` != 0 appends without a header (strips
+ * after the first). */
+int silt_snapshot_to_string(const silt_problem* problem, const double* aos, int64_t j0,
+                            int64_t rows, double time, int header, char* out, int64_t cap,
+                            int64_t* len);
+int silt_write_snapshot(const silt_problem* problem, const double* aos, int64_t j0,
+                        int64_t rows, double time, const char* path, int append,
+                        int64_t* bytes);
+/* the solver's current state (its rows of the grid), straight from the device */
+int silt_solver_write_snapshot(silt_solver* s, double time, const char* path, int append,
+                               int64_t* bytes);
+/* every strip in order: one file for the whole grid */
+int silt_group_write_snapshot(silt_group* g, double time, const char* path, int64_t* bytes);
 
 /* ---- one-shot conveniences (mirror the reference free functions) ---------- */
 /* run_serial: whole run on one GPU; host AoS in/out; dt_log may be NULL. */

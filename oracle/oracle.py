@@ -84,6 +84,9 @@ class CpuSolver:
         g = getattr(L, f"{prefix}_law_eval")
         g.argtypes = [_P, _D, _I64, _D]
         self._law = g
+        g = getattr(L, f"{prefix}_snapshot_to_string")
+        g.argtypes = [_P, _D, C.c_double, C.c_char_p, _I64, C.POINTER(_I64)]
+        self._snap = g
         g = getattr(L, f"{prefix}_shields_flux")
         g.argtypes = [C.c_int, _D, _D, _I64, _D]
         self._shields = g
@@ -173,6 +176,16 @@ class CpuSolver:
         out = np.empty((states.shape[0], 6))
         self._check(self._law(C.byref(problem), _dp(states), states.shape[0], _dp(out)))
         return out
+
+    def snapshot_to_string(self, problem, field, time: float) -> bytes:
+        """snapshot_to_string (src/snapshot.cpp:50-84) of a whole-grid field."""
+        field = np.ascontiguousarray(field, dtype=np.float64)
+        n = _I64(0)
+        self._check(self._snap(C.byref(problem), _dp(field), float(time), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        self._check(self._snap(C.byref(problem), _dp(field), float(time), buf, n.value,
+                               C.byref(n)))
+        return buf.raw[:n.value]
 
     def shields_flux(self, formula: int, tau, tau_cr) -> np.ndarray:
         """(n, 2): shields_flux, shields_flux_derivative."""

@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include "silt/io.hpp"
 #include "silt/parallel.hpp"
 #include "silt/relax_state.hpp"
 #include "silt/riemann.hpp"
@@ -379,6 +380,19 @@ int ref_shields_flux(int formula, const double* tau, const double* tau_cr, int64
             out[2 * k] = shields_flux(f, tau[k], tau_cr[k]);
             out[2 * k + 1] = shields_flux_derivative(f, tau[k], tau_cr[k]);
         }
+    });
+}
+
+// snapshot_to_string (src/snapshot.cpp:50-84) of an AoS field; *len = bytes
+// needed; copies min(len, cap) bytes into out.
+int ref_snapshot_to_string(const silt_problem* p, const double* aos, double time, char* out,
+                           int64_t cap, int64_t* len) {
+    return guarded([&] {
+        const Grid g = make_grid(*p);
+        const Field f = make_field(g, aos);
+        const std::string s = snapshot_to_string(f, time, make_phys(*p));
+        *len = static_cast<int64_t>(s.size());
+        if (out) std::memcpy(out, s.data(), std::min<size_t>(s.size(), (size_t)cap));
     });
 }
 

@@ -1006,3 +1006,60 @@ int orc_shields_flux(int formula, const double* tau, const double* tau_cr, int64
     }
     return 0;
 }
+
+/* snapshot_to_string: src/snapshot.cpp:14-18 (append_num), 50-84.  *len = bytes
+ * needed; min(len, cap) bytes are copied into out. */
+int orc_snapshot_to_string(const silt_problem* p, const double* aos, double time, char* out,
+                           int64_t cap, int64_t* len) {
+    const grid_t g = make_grid(p);
+    int64_t used = 0;
+    char buf[64];
+#define ORC_PUT(str)                                                         \
+    do {                                                                     \
+        const char* s_ = (str);                                              \
+        const size_t n_ = strlen(s_);                                        \
+        if (out && used + (int64_t)n_ <= cap) memcpy(out + used, s_, n_);    \
+        used += (int64_t)n_;                                                 \
+    } while (0)
+#define ORC_NUM(v)                                  \
+    do {                                            \
+        snprintf(buf, sizeof buf, "%.17g", (v));    \
+        ORC_PUT(buf);                               \
+    } while (0)
+    ORC_PUT(g.dim == 1 ? "x,h,u,zb,eta,time\n" : "x,y,h,u,v,zb,eta,time\n");
+    for (int j = 0; j < g.ny; ++j) {
+        for (int i = 0; i < g.nx; ++i) {
+            const double* c = aos + 4 * ((size_t)j * g.nx + i);
+            cell_t s;
+            s.h = c[0];
+            s.hu = c[1];
+            s.hv = c[2];
+            s.zb = c[3];
+            const prim_t pr = primitives(s, g.P.h_dry);
+            ORC_NUM((i + 0.5) * g.dx);
+            ORC_PUT(",");
+            if (g.dim == 2) {
+                ORC_NUM((j + 0.5) * g.dy);
+                ORC_PUT(",");
+            }
+            ORC_NUM(s.h);
+            ORC_PUT(",");
+            ORC_NUM(pr.u);
+            ORC_PUT(",");
+            if (g.dim == 2) {
+                ORC_NUM(pr.v);
+                ORC_PUT(",");
+            }
+            ORC_NUM(s.zb);
+            ORC_PUT(",");
+            ORC_NUM(s.h + s.zb);
+            ORC_PUT(",");
+            ORC_NUM(time);
+            ORC_PUT("\n");
+        }
+    }
+#undef ORC_NUM
+#undef ORC_PUT
+    *len = used;
+    return 0;
+}

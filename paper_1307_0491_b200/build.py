@@ -2,9 +2,10 @@
 
     python -m paper_1307_0491_b200.build        # or __graft_entry__.build()
 
-Three translation units:
+Four translation units:
   csrc/silt_fast.cu    FAST kernels   (-fmad=true)
   csrc/silt_strict.cu  STRICT kernels (-fmad=false: reference operation order)
+  csrc/silt_csv.cu     snapshot CSV formatting kernels (-fmad=false)
   csrc/silt_capi.cu    host runtime behind include/silt_cuda.h
 linked with nvcc into paper_1307_0491_b200/lib/libsilt_b200.so (static cudart).
 """
@@ -29,6 +30,7 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + INCLUD
 UNITS = [
     ("silt_fast.cu", ["-fmad=true"]),
     ("silt_strict.cu", ["-fmad=false"]),
+    ("silt_csv.cu", ["-fmad=false"]),
     ("silt_capi.cu", []),
 ]
 

@@ -15,6 +15,11 @@
 #include <string>
 #include <vector>
 
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "silt_csv_launch.h"
 #include "silt_cuda.h"
 #include "silt_launch.h"
 #include "silt_layout.h"
@@ -1111,6 +1116,279 @@ int silt_selftest_math(const double* x, const double* y, int64_t n, double* out)
     cudaFree(dy);
     cudaFree(dout);
     if (e != cudaSuccess) return fail(SILT_ERR_CUDA, cudaGetErrorString(e));
+    return SILT_OK;
+}
+
+}  // extern "C"
+
+// ---- snapshot CSV (write_snapshot / snapshot_to_string on the device) -------
+// src/snapshot.cpp:50-93.  Chunks of rows are formatted by silt_csv.cu into
+// device memory, copied into one of two pinned host buffers and handed to the
+// sink (file or memory) while the next chunk is formatted.
+
+namespace {
+
+struct CsvSink {
+    FILE* fp = nullptr;         // file sink
+    char* mem = nullptr;        // memory sink
+    int64_t cap = 0, used = 0;  // memory sink capacity / bytes produced
+    std::string path;
+    bool failed = false;
+    void write(const char* p, size_t n) {
+        if (fp) {
+            if (n && std::fwrite(p, 1, n, fp) != n) failed = true;
+        } else {
+            if (mem && used + (int64_t)n <= cap) std::memcpy(mem + used, p, n);
+        }
+        used += (int64_t)n;
+    }
+};
+
+struct CsvCtx {
+    int device = 0;
+    int chunk_cells = 0;
+    silt_csv::Pow5Table* table = nullptr;
+    char* stage = nullptr;
+    int* len = nullptr;
+    int* off = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
+    char* out = nullptr;
+    double* field = nullptr;  // device copy of host rows
+    char* host[2] = {nullptr, nullptr};
+    int* tail = nullptr;      // pinned: {off[n-1], len[n-1]}
+    cudaStream_t stream = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr};
+};
+
+std::mutex g_csv_mu;
+std::map<int, CsvCtx*> g_csv;
+
+int csv_ctx(int device, CsvCtx** out) {
+    std::lock_guard<std::mutex> lock(g_csv_mu);
+    auto it = g_csv.find(device);
+    if (it != g_csv.end()) {
+        *out = it->second;
+        return SILT_OK;
+    }
+    CUDA_TRY(cudaSetDevice(device));
+    auto* c = new CsvCtx();
+    c->device = device;
+    c->chunk_cells = 1 << 21;
+    const size_t n = (size_t)c->chunk_cells;
+    silt_csv::Pow5Table host_table;
+    silt_csv::build_pow5(host_table);
+    CUDA_TRY(cudaMalloc(&c->table, sizeof(silt_csv::Pow5Table)));
+    CUDA_TRY(cudaMemcpy(c->table, &host_table, sizeof host_table, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&c->stage, n * kCsvRowMax));
+    CUDA_TRY(cudaMalloc(&c->len, n * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&c->off, n * sizeof(int)));
+    c->temp_bytes = silt_csv_scan_temp_bytes((int)n);
+    CUDA_TRY(cudaMalloc(&c->temp, c->temp_bytes));
+    CUDA_TRY(cudaMalloc(&c->out, n * kCsvRowMax));
+    CUDA_TRY(cudaMalloc(&c->field, 4 * n * sizeof(double)));
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(cudaHostAlloc(&c->host[b], n * kCsvRowMax, cudaHostAllocPortable));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->copied[b], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaHostAlloc(&c->tail, 2 * sizeof(int), cudaHostAllocPortable));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    g_csv[device] = c;
+    *out = c;
+    return SILT_OK;
+}
+
+// rows [0, rows) of field F (device) -> CSV; F may instead be host AoS
+// (host_aos != nullptr), copied chunk by chunk.
+int csv_emit(int device, CsvField F, const double* host_aos, const silt_problem& p, int rows,
+             int j0, double time, bool header, CsvSink& sink) {
+    CsvCtx* c = nullptr;
+    if (int rc = csv_ctx(device, &c)) return rc;
+    std::lock_guard<std::mutex> lock(g_csv_mu);  // one emitter per process at a time
+    CUDA_TRY(cudaSetDevice(device));
+    const int dim = p.dim;
+    if (header) {
+        const char* h = dim == 1 ? "x,h,u,zb,eta,time\n" : "x,y,h,u,v,zb,eta,time\n";
+        sink.write(h, std::strlen(h));
+    }
+    const int nx = p.nx;
+    int chunk_cells = c->chunk_cells;
+    if (const char* e = std::getenv("SILT_CSV_CHUNK"))  // smaller chunks (tests)
+        chunk_cells = std::max(1, std::min(chunk_cells, std::atoi(e)));
+    const int crow = std::max(1, chunk_cells / nx);
+    if ((long long)nx > chunk_cells)
+        return fail(SILT_ERR_UNSUPPORTED, "write_snapshot: rows longer than the chunk size");
+    int pending = -1;  // host buffer holding the previous chunk
+    int64_t pending_bytes = 0;
+    for (int r0 = 0, chunk = 0; r0 < rows; r0 += crow, ++chunk) {
+        const int nr = std::min(crow, rows - r0);
+        const int n = nr * nx;
+        CsvField G = F;
+        if (host_aos) {
+            CUDA_TRY(cudaMemcpyAsync(c->field, host_aos + 4 * (size_t)r0 * nx,
+                                     4 * (size_t)n * sizeof(double), cudaMemcpyHostToDevice,
+                                     c->stream));
+            for (int f = 0; f < 4; ++f) G.f[f] = c->field + f;
+            G.row_stride = 4LL * nx;
+            G.col_stride = 4;
+        } else {
+            for (int f = 0; f < 4; ++f) G.f[f] = F.f[f] + (long long)r0 * F.row_stride;
+        }
+        CsvGeom geo{nx, nr, j0 + r0, dim, p.dx, p.dy, p.h_dry, time};
+        silt_csv_format_launch(G, geo, c->table, c->stage, c->len, c->stream);
+        silt_csv_scan(c->len, c->off, n, c->temp, c->temp_bytes, c->stream);
+        silt_csv_compact_launch(c->stage, c->len, c->off, n, c->out, c->stream);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(&c->tail[0], c->off + (n - 1), sizeof(int),
+                                 cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(&c->tail[1], c->len + (n - 1), sizeof(int),
+                                 cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        const int64_t bytes = (int64_t)c->tail[0] + c->tail[1];
+        const int b = chunk & 1;
+        CUDA_TRY(cudaMemcpyAsync(c->host[b], c->out, (size_t)bytes, cudaMemcpyDeviceToHost,
+                                 c->stream));
+        CUDA_TRY(cudaEventRecord(c->copied[b], c->stream));
+        if (pending >= 0) {  // the host writes chunk k-1 while chunk k is copied
+            CUDA_TRY(cudaEventSynchronize(c->copied[pending]));
+            sink.write(c->host[pending], (size_t)pending_bytes);
+        }
+        pending = b;
+        pending_bytes = bytes;
+        // the next chunk's compaction overwrites c->out: order it after this copy
+    }
+    if (pending >= 0) {
+        CUDA_TRY(cudaEventSynchronize(c->copied[pending]));
+        sink.write(c->host[pending], (size_t)pending_bytes);
+    }
+    return SILT_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+CsvField aos_field(const double* aos, int nx) {
+    CsvField F;
+    for (int f = 0; f < 4; ++f) F.f[f] = aos + f;
+    F.row_stride = 4LL * nx;
+    F.col_stride = 4;
+    return F;
+}
+
+int open_sink(CsvSink& sink, const char* path, bool append) {
+    sink.path = path;
+    sink.fp = std::fopen(path, append ? "ab" : "wb");
+    if (!sink.fp)
+        return fail(SILT_ERR_RUNTIME, std::string("cannot open '") + path + "' for writing");
+    return SILT_OK;
+}
+
+int close_sink(CsvSink& sink, int rc) {
+    if (sink.fp) {
+        if (std::fclose(sink.fp) != 0) sink.failed = true;
+        sink.fp = nullptr;
+    }
+    if (rc) return rc;
+    if (sink.failed) return fail(SILT_ERR_RUNTIME, "failed writing '" + sink.path + "'");
+    return SILT_OK;
+}
+
+int check_rows(const silt_problem* p, int64_t j0, int64_t rows) {
+    if (int rc = validate_problem(p)) return rc;
+    const int64_t gny = p->dim == 1 ? 1 : p->ny;
+    if (j0 < 0 || rows < 0 || j0 + rows > gny)
+        return fail(SILT_ERR_INVALID, "write_snapshot: rows outside the grid");
+    return SILT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int silt_snapshot_to_string(const silt_problem* problem, const double* aos, int64_t j0,
+                            int64_t rows, double time, int header, char* out, int64_t cap,
+                            int64_t* len) {
+    if (!aos || !len) return fail(SILT_ERR_INVALID, "silt_snapshot_to_string: null argument");
+    if (int rc = check_rows(problem, j0, rows)) return rc;
+    const bool dev = is_device_ptr(aos);
+    int device = 0;
+    if (dev) {
+        cudaPointerAttributes a{};
+        CUDA_TRY(cudaPointerGetAttributes(&a, aos));
+        device = a.device;
+    }
+    CsvSink sink;
+    sink.mem = out;
+    sink.cap = out ? cap : 0;
+    const int rc = csv_emit(device, aos_field(dev ? aos : nullptr, problem->nx),
+                            dev ? nullptr : aos, *problem, (int)rows, (int)j0, time, header != 0,
+                            sink);
+    *len = sink.used;
+    if (rc) return rc;
+    if (sink.used > sink.cap)
+        return fail(SILT_ERR_INVALID, "silt_snapshot_to_string: buffer too small (see *len)");
+    return SILT_OK;
+}
+
+int silt_write_snapshot(const silt_problem* problem, const double* aos, int64_t j0, int64_t rows,
+                        double time, const char* path, int append, int64_t* bytes) {
+    if (!aos || !path) return fail(SILT_ERR_INVALID, "silt_write_snapshot: null argument");
+    if (int rc = check_rows(problem, j0, rows)) return rc;
+    const bool dev = is_device_ptr(aos);
+    int device = 0;
+    if (dev) {
+        cudaPointerAttributes a{};
+        CUDA_TRY(cudaPointerGetAttributes(&a, aos));
+        device = a.device;
+    }
+    CsvSink sink;
+    if (int rc = open_sink(sink, path, append != 0)) return rc;
+    int rc = csv_emit(device, aos_field(dev ? aos : nullptr, problem->nx), dev ? nullptr : aos,
+                      *problem, (int)rows, (int)j0, time, append == 0, sink);
+    rc = close_sink(sink, rc);
+    if (bytes) *bytes = sink.used;
+    return rc;
+}
+
+int silt_solver_write_snapshot(silt_solver* s, double time, const char* path, int append,
+                               int64_t* bytes) {
+    if (!s || !path) return fail(SILT_ERR_INVALID, "silt_solver_write_snapshot: null argument");
+    int p = 0;
+    if (s->begun) {
+        Slot sl;
+        if (int rc = read_slot(s, &sl, nullptr)) return rc;
+        p = (int)(sl.steps & 1);
+    } else {
+        CUDA_TRY(cudaSetDevice(s->device));
+        CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    CsvField F;
+    for (int f = 0; f < 4; ++f) F.f[f] = s->args.state[p][f];
+    F.row_stride = s->pitch;
+    F.col_stride = 1;
+    CsvSink sink;
+    if (int rc = open_sink(sink, path, append != 0)) return rc;
+    int rc = csv_emit(s->device, F, nullptr, s->prob, s->ny, s->strip.j0, time, append == 0, sink);
+    rc = close_sink(sink, rc);
+    if (bytes) *bytes = sink.used;
+    return rc;
+}
+
+int silt_group_write_snapshot(silt_group* g, double time, const char* path, int64_t* bytes) {
+    if (!g || !path) return fail(SILT_ERR_INVALID, "silt_group_write_snapshot: null argument");
+    int64_t total = 0;
+    for (size_t k = 0; k < g->strips.size(); ++k) {
+        int64_t b = 0;
+        if (int rc = silt_solver_write_snapshot(g->strips[k], time, path, k > 0, &b)) return rc;
+        total += b;
+    }
+    if (bytes) *bytes = total;
     return SILT_OK;
 }
 

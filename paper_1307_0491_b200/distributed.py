@@ -22,6 +22,7 @@ object that implements the strip-solver interface below.
 """
 from __future__ import annotations
 
+import ctypes as C
 import os
 
 import numpy as np
@@ -409,6 +410,13 @@ class LocalStripGroup:
 
     def capture_wait(self):
         self.N.check(self.L.silt_group_capture_wait(self.h))
+
+    def write_snapshot(self, time: float, path: str) -> int:
+        """Whole-grid CSV (write_snapshot), every strip formatted on its device."""
+        n = C.c_int64(0)
+        self.N.check(self.L.silt_group_write_snapshot(self.h, float(time), os.fsencode(path),
+                                                      C.byref(n)))
+        return n.value
 
     def run(self, batch: int = 8, on_snapshot=None, async_snapshots: bool = False):
         return self.N._run_loop(self.step, self.status, self.resume, self.gather,

@@ -99,6 +99,14 @@ def lib() -> C.CDLL:
         "silt_solver_capture_query": ([_VP, C.POINTER(C.c_int)], C.c_int),
         "silt_host_alloc": ([C.c_int64, C.POINTER(_VP)], C.c_int),
         "silt_host_free": ([_VP], C.c_int),
+        "silt_snapshot_to_string": ([_P, _VP, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                     C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+        "silt_write_snapshot": ([_P, _VP, C.c_int64, C.c_int64, C.c_double, C.c_char_p,
+                                 C.c_int, C.POINTER(C.c_int64)], C.c_int),
+        "silt_solver_write_snapshot": ([_VP, C.c_double, C.c_char_p, C.c_int,
+                                        C.POINTER(C.c_int64)], C.c_int),
+        "silt_group_write_snapshot": ([_VP, C.c_double, C.c_char_p, C.POINTER(C.c_int64)],
+                                      C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -311,6 +319,13 @@ class Solver:
     def capture_wait(self):
         check(self.L.silt_solver_capture_wait(self.h))
 
+    def write_snapshot(self, time: float, path: str, append: bool = False) -> int:
+        """CSV of the current state (write_snapshot) formatted on the device."""
+        n = C.c_int64(0)
+        check(self.L.silt_solver_write_snapshot(self.h, float(time), os.fsencode(path),
+                                                int(append), C.byref(n)))
+        return n.value
+
     def run(self, batch: int = 32, on_snapshot=None, async_snapshots: bool = False) -> SiltStatus:
         """Advance until DONE; PAUSED snapshots call on_snapshot(t, field)."""
         return _run_loop(self.step, self.status, self.resume, self.download,
@@ -357,6 +372,46 @@ def faces(problem: SiltProblem, left: np.ndarray, right: np.ndarray, axis: int,
     check(lib().silt_riemann_batch(C.byref(problem), _dp(left), _dp(right), left.shape[0],
                                    axis, variant, _dp(out)))
     return out
+
+
+def _field_ptr(field, problem: SiltProblem, rows):
+    """(pointer, rows) of a host ndarray or a device pointer (int, needs rows)."""
+    if isinstance(field, np.ndarray):
+        field = np.ascontiguousarray(field, dtype=np.float64)
+        n = field.size // (4 * problem.nx)
+        return field, field.ctypes.data, (n if rows is None else rows)
+    if rows is None:
+        raise ValueError("rows is required for a device pointer")
+    return None, int(field), rows
+
+
+def snapshot_to_string(problem: SiltProblem, field, time: float, *, j0: int = 0,
+                       rows: int | None = None, header: bool = True) -> bytes:
+    """snapshot_to_string (reference src/snapshot.cpp:50-84), formatted on the GPU.
+    ``field``: AoS rows [j0, j0 + rows) — a numpy array or a device pointer."""
+    keep, ptr, rows = _field_ptr(field, problem, rows)
+    n = C.c_int64(0)
+    rc = lib().silt_snapshot_to_string(C.byref(problem), ptr, j0, rows, float(time),
+                                       int(header), None, 0, C.byref(n))
+    if rc not in (abi.SILT_OK, abi.SILT_ERR_INVALID) or (rc and n.value == 0):
+        check(rc)
+    buf = C.create_string_buffer(max(n.value, 1))
+    check(lib().silt_snapshot_to_string(C.byref(problem), ptr, j0, rows, float(time),
+                                        int(header), buf, n.value, C.byref(n)))
+    del keep
+    return buf.raw[:n.value]
+
+
+def write_snapshot(problem: SiltProblem, field, time: float, path: str, *, j0: int = 0,
+                   rows: int | None = None, append: bool = False) -> int:
+    """write_snapshot (reference src/snapshot.cpp:86-93), formatted on the GPU;
+    returns the bytes written."""
+    keep, ptr, rows = _field_ptr(field, problem, rows)
+    n = C.c_int64(0)
+    check(lib().silt_write_snapshot(C.byref(problem), ptr, j0, rows, float(time),
+                                    os.fsencode(path), int(append), C.byref(n)))
+    del keep
+    return n.value
 
 
 def law_terms(problem: SiltProblem, states: np.ndarray,
