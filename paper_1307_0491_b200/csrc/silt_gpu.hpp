@@ -10,6 +10,7 @@
 //   silt::step_1d/2d  (include/silt/stepper.hpp:47-54)   -> silt::gpu::step_1d/2d
 //   silt::run_serial  (include/silt/parallel.hpp:80)     -> silt::gpu::run_serial
 //   silt::run_parallel(include/silt/parallel.hpp:85-86)  -> silt::gpu::run_parallel
+//   silt::write_snapshot / snapshot_to_string (io.hpp:69-73) -> silt::gpu::write_snapshot / ...
 //
 // Same argument meaning, same exception classes and messages:
 // std::invalid_argument for preconditions, std::runtime_error for numerical
@@ -228,6 +229,29 @@ inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
 }
 
 }  // namespace detail
+
+// snapshot_to_string / write_snapshot (include/silt/io.hpp:69-73), formatted
+// on the GPU (silt_csv.cu): the same bytes as the reference's.
+inline std::string snapshot_to_string(const Field& f, double time, const Physics& phys = {}) {
+    silt_problem p = detail::problem(f.grid, BedloadLaw::grass(0.0), phys, 0.5, 1.0);
+    const int64_t rows = f.grid.dim == 1 ? 1 : f.grid.ny;
+    int64_t len = 0;
+    const int rc = silt_snapshot_to_string(&p, detail::data(f.cells), 0, rows, time, 1, nullptr,
+                                           0, &len);
+    if (rc != SILT_OK && !(rc == SILT_ERR_INVALID && len > 0)) check(rc);
+    std::string out(static_cast<size_t>(len), '\0');
+    check(silt_snapshot_to_string(&p, detail::data(f.cells), 0, rows, time, 1, out.data(), len,
+                                  &len));
+    return out;
+}
+
+inline void write_snapshot(const Field& f, double time, const std::string& path,
+                           const Physics& phys = {}) {
+    silt_problem p = detail::problem(f.grid, BedloadLaw::grass(0.0), phys, 0.5, 1.0);
+    const int64_t rows = f.grid.dim == 1 ? 1 : f.grid.ny;
+    check(silt_write_snapshot(&p, detail::data(f.cells), 0, rows, time, path.c_str(), 0,
+                              nullptr));
+}
 
 // run_serial (include/silt/parallel.hpp:80)
 inline RunResult run_serial(const Scenario& sc, const RunOptions& opt = {}) {

@@ -3,6 +3,7 @@
 // reference's doctest suites (proj/tests/test_stepper.cpp, test_parallel.cpp).
 // Linked with oracle/_ref/libsilt_ref.so (the unmodified reference core) for
 // the scenario builders and the CPU run_serial it is compared with.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -10,6 +11,11 @@
 #include <string>
 #include <vector>
 
+#include <fstream>
+#include <sstream>
+#include <stdlib.h>
+
+#include "silt/io.hpp"
 #include "silt/parallel.hpp"
 #include "silt/scenarios.hpp"
 #include "silt/stepper.hpp"
@@ -159,8 +165,73 @@ static void test_runs(int variant) {
     CHECK(throws<std::invalid_argument>([&] { gpu::run_serial(neg, bad); }));
 }
 
+static std::string slurp(const std::string& path) {
+    std::ifstream is(path, std::ios::binary);
+    std::stringstream ss;
+    ss << is.rdbuf();
+    return ss.str();
+}
+
+// The CLI's simulate / bench-speedup flow (tools/src/main.cpp:100-203,
+// 261-317) with silt::run_parallel swapped for silt::gpu::run_parallel and
+// write_snapshot for silt::gpu::write_snapshot: snapshot files byte-identical
+// to the CPU flow's (STRICT), timing.csv / speedup.csv from the reference's
+// own report writers.
+static void test_cli_flow() {
+    char tmpl[] = "/tmp/silt_shim_XXXXXX";
+    const std::string dir = mkdtemp(tmpl);
+    const Scenario sc = build_bump_2d(64, 48, 1.0);
+    RunOptions opt;
+    opt.max_steps = 50;
+    opt.snapshot_times = {0.0, 2.0, 4.0};
+    int k_ref = 0, k_gpu = 0;
+    opt.on_snapshot = [&](double t, const Field& f) {
+        write_snapshot(f, t, dir + "/ref_" + std::to_string(k_ref++) + ".csv", sc.phys);
+    };
+    const RunResult ref = run_parallel(sc, 1, 2, opt);
+    gpu::variant() = SILT_VARIANT_STRICT;
+    opt.on_snapshot = [&](double t, const Field& f) {
+        gpu::write_snapshot(f, t, dir + "/gpu_" + std::to_string(k_gpu++) + ".csv", sc.phys);
+    };
+    const RunResult got = gpu::run_parallel(sc, 1, 2, opt);
+    CHECK(k_ref == 3 && k_gpu == 3);
+    for (int k = 0; k < 3; ++k) {
+        const std::string a = slurp(dir + "/ref_" + std::to_string(k) + ".csv");
+        const std::string b = slurp(dir + "/gpu_" + std::to_string(k) + ".csv");
+        CHECK(!a.empty() && a == b);
+    }
+    CHECK(snapshot_to_string(got.final_field, got.time, sc.phys) ==
+          gpu::snapshot_to_string(got.final_field, got.time, sc.phys));
+    gpu::write_snapshot(got.final_field, got.time, dir + "/final_gpu.csv", sc.phys);
+    write_snapshot(ref.final_field, ref.time, dir + "/final_ref.csv", sc.phys);
+    CHECK(slurp(dir + "/final_gpu.csv") == slurp(dir + "/final_ref.csv"));
+    // timing.csv: one row per worker strip, the reference's writer
+    const std::string timing = timing_to_csv(got.timing);
+    CHECK(timing.rfind("rank,steps,compute_seconds,exchange_seconds\n", 0) == 0);
+    CHECK(std::count(timing.begin(), timing.end(), '\n') == 3);
+    CHECK(timing.find("\n1,50,") != std::string::npos);
+    // bench-speedup: layouts 1x1 and 1x2 on the GPU runner
+    gpu::variant() = SILT_VARIANT_FAST;
+    RunOptions bo;
+    bo.max_steps = 20;
+    std::vector<std::pair<int, double>> timings;
+    for (int py : {1, 2}) timings.emplace_back(py, gpu::run_parallel(sc, 1, py, bo).wall_seconds);
+    const std::vector<SpeedupRow> rows = speedup_report(timings, 1);
+    const std::string csv = speedup_to_csv(rows);
+    CHECK(csv.rfind("workers,seconds,speedup,efficiency\n1,", 0) == 0);
+    CHECK(rows.size() == 2 && rows[0].speedup == 1.0);
+    std::remove((dir + "/final_gpu.csv").c_str());
+    std::remove((dir + "/final_ref.csv").c_str());
+    for (int k = 0; k < 3; ++k) {
+        std::remove((dir + "/ref_" + std::to_string(k) + ".csv").c_str());
+        std::remove((dir + "/gpu_" + std::to_string(k) + ".csv").c_str());
+    }
+    std::remove(dir.c_str());
+}
+
 int main() {
     test_cfl();
+    test_cli_flow();
     test_steps_match_reference();
     test_runs(SILT_VARIANT_STRICT);
     test_runs(SILT_VARIANT_FAST);
