@@ -324,6 +324,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     }
     for (int p = 0; p < 2; ++p)
         for (int f = 0; f < 4; ++f) A.state[p][f] = s->planes + (size_t)(p * 4 + f) * plane;
+    A.plane = (long long)plane;
     const size_t row = 4 * (size_t)s->nx;
     A.ghost_s[0] = s->rows + 0 * row;
     A.ghost_s[1] = s->rows + 1 * row;
@@ -344,8 +345,25 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     if (problem->dim == 1) R = 1;
     A.rows_per_block = (int)R;
     const int warps_per_cta = kStepThreads / 32;
-    s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta),
-                        (unsigned)((s->ny + R - 1) / R), 1);
+    // 2D: row block = 8 * blockIdx.y + blockIdx.z.  Blocks are issued z
+    // slowest, so the launch sweeps the domain 8 times, each pass taking every
+    // 8th row block: the blocks through a localised active region (C4's
+    // mound) are spread over the whole launch instead of forming one
+    // compute-bound window in which the memory-bound quiescent blocks starve.
+    // Columns stay fastest (x-halo sharing in L2); surplus blocks (< 8) exit.
+    // Only for launches of many waves (>= 64 CTAs per SM): in short launches
+    // the interleave costs the row-halo sharing in L2 and buys nothing.
+    {
+        const unsigned nb = (unsigned)((s->ny + R - 1) / R);
+        const long long ctas = (long long)nb * ((strips + warps_per_cta - 1) / warps_per_cta);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const char* e = std::getenv("SILT_ROW_PERM");
+        const bool perm = e ? e[0] != '0' : ctas >= 64LL * sms;
+        const unsigned gz = (problem->dim == 2 && nb >= 16 && perm) ? 8u : 1u;
+        s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta),
+                            (nb + gz - 1) / gz, gz);
+    }
     if (cudaDeviceSynchronize() != cudaSuccess)
         return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: init failed"));
     *out = s;

@@ -358,8 +358,9 @@ __device__ __forceinline__ void make_sides(const StepArgs& A, const double c[4],
 // interior rows then cost one multiply-add per field.  Rows -1 / ny come from
 // the ghost-row buffers (physical BC rows, or rows received from a neighbour).
 struct RowSrc {
-    const double* base[4];
-    size_t stride;  // row stride of base (pitch, or 1 for a given ghost column)
+    const double* base;  // field 0; field f at base + f * fstride
+    size_t stride;       // row stride (pitch, or 1 for a given ghost column)
+    size_t fstride;      // field stride (plane, or ny for a given ghost column)
     int col_clamped;
 };
 
@@ -374,7 +375,8 @@ __device__ __forceinline__ RowSrc row_src(const StepArgs& A, int p, int col) {
         if (t == SILT_BC_GIVEN) {
             const double* g = side == SILT_WEST ? A.ghost_w : A.ghost_e;
 #pragma unroll
-            for (int f = 0; f < 4; ++f) s.base[f] = g + (size_t)f * A.ny;
+            s.base = g;
+            s.fstride = A.ny;
             s.stride = 1;
             s.col_clamped = col < 0 ? 0 : nx - 1;
             return s;
@@ -383,15 +385,15 @@ __device__ __forceinline__ RowSrc row_src(const StepArgs& A, int p, int col) {
     } else {
         c = min(max(col, 0), nx - 1);  // dead lanes: any valid cell
     }
-#pragma unroll
-    for (int f = 0; f < 4; ++f) s.base[f] = A.state[p][f] + c;
+    s.base = A.state[p][0] + c;
+    s.fstride = A.plane;
     s.col_clamped = min(max(col, 0), nx - 1);
     return s;
 }
 
 __device__ __forceinline__ const double* row_field(const StepArgs& A, const RowSrc& s, int p,
                                                    int row, int f) {
-    if (row >= 0 && row < A.ny) return s.base[f] + (size_t)row * s.stride;
+    if (row >= 0 && row < A.ny) return s.base + (size_t)f * s.fstride + (size_t)row * s.stride;
     const double* g = row < 0 ? (A.south_nbr ? A.recv_s : A.ghost_s[p])
                               : (A.north_nbr ? A.recv_n : A.ghost_n[p]);
     return g + (size_t)f * A.nx + s.col_clamped;
@@ -410,7 +412,8 @@ __device__ __forceinline__ void prefetch_row(const StepArgs& A, const RowSrc& s,
     if (row >= 0 && row < A.ny) {
         const size_t off = (size_t)row * s.stride;
 #pragma unroll
-        for (int f = 0; f < 4; ++f) cp_async8_s(dst + f * kFieldBytes, s.base[f] + off);
+        for (int f = 0; f < 4; ++f)
+            cp_async8_s(dst + f * kFieldBytes, s.base + (size_t)f * s.fstride + off);
     } else {
 #pragma unroll
         for (int f = 0; f < 4; ++f) cp_async8_s(dst + f * kFieldBytes, row_field(A, s, p, row, f));
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const int col = i0 - 1 + lane;
     const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < A.nx;
     const bool xface = lane <= kCellsPerWarp && col <= A.nx - 1;  // face at right of col
-    const int jb = blockIdx.y * A.rows_per_block;
+    const int jb = (blockIdx.y * gridDim.z + blockIdx.z) * A.rows_per_block;
     const int je = min(jb + A.rows_per_block, A.ny);
     if (jb >= je) return;
     const double cx = d.dt / A.dx;
@@ -556,10 +559,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     Reduce R{0.0, 0.0, 0.0, 0u};
     const unsigned row_sa0 = (unsigned)__cvta_generic_to_shared(&sh_row[0][0][t]);
     constexpr unsigned kSlotBytes = 4 * kStepThreads * sizeof(double);
-    double* const out0 = A.state[q][0] + col;  // output cell (row 0) of each field
-    double* const out1 = A.state[q][1] + col;
-    double* const out2 = A.state[q][2] + col;
-    double* const out3 = A.state[q][3] + col;
+    double* const out0 = A.state[q][0] + col;  // output cell (row 0) of field 0
+    const size_t plane = A.plane;              // field f at out0 + f * plane
 #pragma unroll
     for (int k = 0; k < SILT_RING - 1; ++k) {
         if (jb - 1 + k <= je) prefetch_row(A, src, p, jb - 1 + k, row_sa0 + k * kSlotBytes);
@@ -626,9 +627,9 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                     if (owned) {  // row r-1 is unchanged: o == c
                         const size_t off = (size_t)(r - 1) * A.pitch;
                         out0[off] = c[0];
-                        out1[off] = c[1];
-                        out2[off] = c[2];
-                        out3[off] = c[3];
+                        out0[off + plane] = c[1];
+                        out0[off + 2 * plane] = c[2];
+                        out0[off + 3 * plane] = c[3];
                         if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, c);
                         if (!qvalid) {  // first row of the streak: its speeds, folded once
                             cell_speeds<S, SH>(A, c, qsx, qsy);
@@ -667,9 +668,9 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
             const size_t off = (size_t)(r - 1) * A.pitch;
             out0[off] = o[0];
-            out1[off] = o[1];
-            out2[off] = o[2];
-            out3[off] = o[3];
+            out0[off + plane] = o[1];
+            out0[off + 2 * plane] = o[2];
+            out0[off + 3 * plane] = o[3];
             if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, o);
             double ssx, ssy;
             cell_speeds<S, SH>(A, o, ssx, ssy);

@@ -59,6 +59,7 @@ struct StepArgs {
     int south_nbr, north_nbr, per_y_self;
     int write_edges_in_reduce;
     int quiet_skip;         // FAST: skip provably unchanged quiescent rows
+    long long plane;        // doubles between the field planes of one parity
     double dx, dy, cfl;
     silt_dev::Params P;
     int bc_type[4];
