@@ -360,7 +360,9 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const char* e = std::getenv("SILT_ROW_PERM");
         const bool perm = e ? e[0] != '0' : ctas >= 64LL * sms;
-        const unsigned gz = (problem->dim == 2 && nb >= 16 && perm) ? 8u : 1u;
+        unsigned passes = 8;
+        if (const char* ep = std::getenv("SILT_ROW_PASSES")) passes = (unsigned)std::max(1, std::atoi(ep));
+        const unsigned gz = (problem->dim == 2 && nb >= 2 * passes && perm) ? passes : 1u;
         s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta),
                             (nb + gz - 1) / gz, gz);
     }

@@ -15,7 +15,10 @@
 #include "silt_cuda.h"
 #include "silt_physics_params.h"
 
-constexpr int kStepThreads = 128;   // 4 warps per CTA, one column strip each
+#ifndef SILT_STEP_THREADS
+#define SILT_STEP_THREADS 128
+#endif
+constexpr int kStepThreads = SILT_STEP_THREADS;  // warps per CTA x 32, one column strip each
 constexpr int kCellsPerWarp = 30;   // lanes 1..30 own cells, 0/31 are x-halo
 
 // One mailbox per launch index mod 3.  Launch n reads slot[n%3] (state n's
