@@ -647,7 +647,7 @@ __device__ __forceinline__ Eval fo_eval(const FluidCtx& c, double m2, double m4)
     }
     e.d = m4 - m2;
     e.valid = e.t1 > 0 && e.t2 > 0 && e.t3 > 0 && e.t4 > 0 && e.d > 0;
-    e.dzl = e.dzr = e.r1 = e.r2 = e.id = 0.0;
+    // the other fields of an invalid evaluation are never read
     if (!e.valid) return e;
     if constexpr (S) {
         e.dzl = (m4 * c.jz - c.jw) / e.d;
