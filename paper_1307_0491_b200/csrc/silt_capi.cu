@@ -71,6 +71,71 @@ __global__ void aos_to_planes(const double* __restrict__ aos, double* planes, in
     for (int f = 0; f < 4; ++f) planes[(size_t)f * n + k] = aos[4 * (size_t)k + f];
 }
 
+// Next launch's row-block order from the hot flags of the launch just
+// enqueued (one CTA; the flags are cleared for reuse).  Hot row blocks go to
+// positions floor((h + 1/2) span / H), span = 0.9 nb, the others fill the
+// remaining positions in row order; without usable information (no hot
+// block, or more than span / 2) the default order is copied.
+__global__ void __launch_bounds__(1024) rb_order_kernel(unsigned char* hot, const int* def,
+                                                        int* lists, int* out, int nb,
+                                                        int span_permille) {
+    __shared__ int s_warp[32];
+    __shared__ int s_base[2];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) s_base[0] = s_base[1] = 0;
+    __syncthreads();
+    int* hot_list = lists;
+    int* cold_list = lists + nb;
+    for (int k0 = 0; k0 < nb; k0 += 1024) {
+        const int k = k0 + t;
+        const int f = (k < nb && hot[k]) ? 1 : 0;
+        // exclusive block scan of f
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int in_warp = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 31) s_warp[w] = in_warp + f;
+        __syncthreads();
+        if (w == 0) {
+            const int v = s_warp[lane];
+            int x = v;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            s_warp[lane] = x - v;  // exclusive
+        }
+        __syncthreads();
+        const int hr = s_base[0] + s_warp[w] + in_warp;  // hot rank
+        if (k < nb) {
+            if (f)
+                hot_list[hr] = k;
+            else
+                cold_list[k - hr] = k;
+            hot[k] = 0;
+        }
+        __syncthreads();
+        if (t == 1023) s_base[0] = hr + f;
+        __syncthreads();
+    }
+    const long long H = s_base[0];
+    const long long span = (long long)nb * span_permille / 1000;
+    const bool use = H > 0 && 2 * H <= span;
+    for (int k = t; k < nb; k += 1024) {
+        if (!use) {
+            out[k] = def[k];
+            continue;
+        }
+        // hot positions before k: #{h : (2h + 1) span < 2 k H}
+        auto before = [&](long long kk) {
+            const long long num = 2 * kk * H - span;
+            if (num <= 0) return 0LL;
+            const long long c = (num + 2 * span - 1) / (2 * span);
+            return c < H ? c : H;
+        };
+        const long long lt = before(k), le = before(k + 1);
+        out[k] = (le > lt) ? hot_list[lt] : cold_list[k - lt];
+    }
+}
+
 int grid_blocks(long long n, int threads) {
     long long b = (n + threads - 1) / threads;
     return (int)std::max(1LL, std::min(b, 148LL * 32));
@@ -94,6 +159,11 @@ struct silt_solver {
     double* cols = nullptr;     // 2 x [4][ny]
     double* staging = nullptr;  // AoS nx*ny*4
     double* snapbuf = nullptr;  // AoS nx*ny*4: device copy of a captured snapshot
+    void* rb_mem = nullptr;     // row-block order: default, lists, 3 tables, 3 hot flags
+    int* rb_default = nullptr;
+    int* rb_lists = nullptr;
+    int row_blocks = 0;
+    int rb_span = 900;          // hot row blocks spread over this share (per mille) of a launch
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
     cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
     bool cap_pending = false;
@@ -199,6 +269,12 @@ void launch_step(silt_solver* s) {
         silt_fast_step(s->args, li, s->step_grid, s->stream);
     ++s->launches;
     ++s->kernel_count;
+    if (s->args.rb_order) {
+        rb_order_kernel<<<1, 1024, 0, s->stream>>>(s->args.rb_hot[li], s->rb_default, s->rb_lists,
+                                                   s->args.rb_table[(li + 1) % 3], s->row_blocks,
+                                                   s->rb_span);
+        ++s->kernel_count;
+    }
 }
 
 int read_slot(silt_solver* s, Slot* out, Control* full) {
@@ -345,26 +421,46 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     if (problem->dim == 1) R = 1;
     A.rows_per_block = (int)R;
     const int warps_per_cta = kStepThreads / 32;
-    // 2D: row block = 8 * blockIdx.y + blockIdx.z.  Blocks are issued z
-    // slowest, so the launch sweeps the domain 8 times, each pass taking every
-    // 8th row block: the blocks through a localised active region (C4's
-    // mound) are spread over the whole launch instead of forming one
-    // compute-bound window in which the memory-bound quiescent blocks starve.
-    // Columns stay fastest (x-halo sharing in L2); surplus blocks (< 8) exit.
-    // Only for launches of many waves (>= 64 CTAs per SM): in short launches
-    // the interleave costs the row-halo sharing in L2 and buys nothing.
+    // 2D row-block launch order (long launches only: >= 64 CTAs per SM; in
+    // short ones the reordering costs the row-halo sharing in L2 and buys
+    // nothing).  Blocks are issued row block by row block, columns fastest
+    // (x-halo sharing in L2).  A row block that does full-path work holds its
+    // SM slots ~10x longer than a quiescent one, so the order spreads the
+    // "hot" row blocks of the previous launch evenly over the first 90 % of
+    // the launch: no window in which compute-bound blocks starve the
+    // memory-bound ones, and none left to start at the end (the tail).
+    // Without hot information the order is 8 interleaved passes (every 8th
+    // row block per pass).  rb_order_kernel rebuilds the order after every
+    // step from the hot flags the step kernel sets.
     {
         const unsigned nb = (unsigned)((s->ny + R - 1) / R);
         const long long ctas = (long long)nb * ((strips + warps_per_cta - 1) / warps_per_cta);
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const char* e = std::getenv("SILT_ROW_PERM");
-        const bool perm = e ? e[0] != '0' : ctas >= 64LL * sms;
-        unsigned passes = 8;
-        if (const char* ep = std::getenv("SILT_ROW_PASSES")) passes = (unsigned)std::max(1, std::atoi(ep));
-        const unsigned gz = (problem->dim == 2 && nb >= 2 * passes && perm) ? passes : 1u;
-        s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta),
-                            (nb + gz - 1) / gz, gz);
+        const bool order = problem->dim == 2 && nb >= 16 && (e ? e[0] != '0' : ctas >= 64LL * sms);
+        s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta), nb, 1);
+        A.rb_order = order ? 1 : 0;
+        if (const char* es = std::getenv("SILT_RB_SPAN")) s->rb_span = std::max(100, std::min(1000, std::atoi(es)));
+        s->row_blocks = (int)nb;
+        if (order) {
+            std::vector<int> def;
+            for (unsigned z = 0; z < 8; ++z)
+                for (unsigned y = z; y < nb; y += 8) def.push_back((int)y);
+            if (cudaMalloc(&s->rb_mem, (4 + 2 * 3) * (size_t)nb * sizeof(int) + 3 * (size_t)nb) !=
+                cudaSuccess)
+                return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: device allocation failed"));
+            int* base = static_cast<int*>(s->rb_mem);
+            s->rb_default = base;
+            s->rb_lists = base + nb;  // hot list, cold list (scratch of the order kernel)
+            for (int k = 0; k < 3; ++k) A.rb_table[k] = base + (size_t)(3 + k) * nb;
+            unsigned char* hot = reinterpret_cast<unsigned char*>(base + (size_t)6 * nb);
+            for (int k = 0; k < 3; ++k) A.rb_hot[k] = hot + (size_t)k * nb;
+            cudaMemset(hot, 0, 3 * (size_t)nb);
+            for (int k = -1; k < 3; ++k)
+                cudaMemcpy(k < 0 ? s->rb_default : A.rb_table[k], def.data(), nb * sizeof(int),
+                           cudaMemcpyHostToDevice);
+        }
     }
     if (cudaDeviceSynchronize() != cudaSuccess)
         return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: init failed"));
@@ -383,6 +479,7 @@ int silt_solver_destroy(silt_solver* s) {
     if (s->cap_ready) cudaEventDestroy(s->cap_ready);
     if (s->cap_done) cudaEventDestroy(s->cap_done);
     cudaFree(s->snapbuf);
+    cudaFree(s->rb_mem);
     cudaFree(s->planes);
     cudaFree(s->rows);
     cudaFree(s->cols);

@@ -518,7 +518,12 @@ struct StepSmem {
     double fy[4][kStepThreads];           // y face below row r-1: h, huR, hv, z
     double row[SILT_RING][4][kStepThreads];  // cp.async ring
     long long cprev[4][kStepThreads];     // previous row (bits), quiescence test
+    int nfull[kStepThreads / 32];         // full-path rows of each warp (launch order)
 };
+
+// Rows of a warp's march on the full (non-quiescent) path above which its
+// row block counts as hot for the next launch's order.
+constexpr int kHotRows = 4;
 
 template <bool S, bool SH>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
@@ -548,9 +553,11 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const int col = i0 - 1 + lane;
     const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < A.nx;
     const bool xface = lane <= kCellsPerWarp && col <= A.nx - 1;  // face at right of col
-    const int jb = (blockIdx.y * gridDim.z + blockIdx.z) * A.rows_per_block;
+    const int jb = (A.rb_order ? __ldg(A.rb_table[li] + blockIdx.y) : (int)blockIdx.y) *
+                   A.rows_per_block;
     const int je = min(jb + A.rows_per_block, A.ny);
     if (jb >= je) return;
+    if (lane == 0) sm.nfull[t >> 5] = 0;
     const double cx = d.dt / A.dx;
     const double cy = d.dt / A.dy;
     const double href = __longlong_as_double((long long)cur.hmax);
@@ -642,6 +649,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             }
         }
 
+        if (own_row && lane == 0) ++sm.nfull[t >> 5];
         // y face between rows r-1 and r (normal = v, transverse = u), solved
         // first; the x-side waits in shared memory for the x face
         Flux fy{0, 0, 0, 0, 0};
@@ -701,6 +709,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         sh_xs[3][t] = c[3] - cx * (fx.z - lz);
         __syncwarp();
     }
+    if (A.rb_order && lane == 0 && sm.nfull[t >> 5] > kHotRows)
+        A.rb_hot[li][__ldg(A.rb_table[li] + blockIdx.y)] = 1;
     reduce_flush(R, nxt);
 }
 

@@ -63,6 +63,12 @@ struct StepArgs {
     int write_edges_in_reduce;
     int quiet_skip;         // FAST: skip provably unchanged quiescent rows
     long long plane;        // doubles between the field planes of one parity
+    // Row-block launch order (2D, long launches): launch li processes row
+    // block rb_table[li][blockIdx.y]; rows with full-path (non-quiescent)
+    // work mark rb_hot[li], from which rb_order_kernel builds the next order.
+    int rb_order;
+    int* rb_table[3];
+    unsigned char* rb_hot[3];
     double dx, dy, cfl;
     silt_dev::Params P;
     int bc_type[4];
