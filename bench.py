@@ -264,6 +264,9 @@ def main():
                                                   refine_partition, row_costs)
 
     world, rank, local = init_dist(args.gpus)
+    # one GPU per rank; ranks beyond the visible devices share them (only for
+    # the one-GPU multi-rank check with SILT_DIST_BACKEND=gloo)
+    local = local % max(1, torch.cuda.device_count())
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     variant = abi.VARIANT_FAST if args.variant == "fast" else abi.VARIANT_STRICT

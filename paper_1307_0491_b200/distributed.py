@@ -138,8 +138,9 @@ def init_dist(gpus: int = 1, backend: str | None = None):
         import torch
         import torch.distributed as dist
         if not dist.is_initialized():
-            if backend is None:
-                backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend is None:  # SILT_DIST_BACKEND=gloo: multi-rank tests on one GPU
+                backend = os.environ.get("SILT_DIST_BACKEND") or (
+                    "nccl" if torch.cuda.is_available() else "gloo")
             kw = {}
             if backend == "nccl":
                 kw["device_id"] = torch.device("cuda", local)
@@ -200,9 +201,14 @@ class StripRunner:
             self.device = None
             self._send_s, self._send_n, self._recv_s, self._recv_n = self.solver.exchange_tensors()
         self._dist = None
+        self._stage = False
         if world > 1:
             import torch.distributed as dist
             self._dist = dist
+            # gloo moves CPU tensors only: device rows are staged through host
+            # memory (used by the one-GPU multi-process tests; NCCL moves the
+            # device buffers directly)
+            self._stage = self.torch_stream is not None and dist.get_backend() == "gloo"
 
     def _wrap(self, ptr, n):
         if not ptr:
@@ -223,6 +229,8 @@ class StripRunner:
         north — consistent pairing also when south == north (periodic, G=2)."""
         if self.world == 1:
             return
+        if self._stage:
+            return self._exchange_staged()
         dist = self._dist
         ops = []
         if self.north is not None:
@@ -237,6 +245,36 @@ class StripRunner:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         dist.all_reduce(self._slot(), op=dist.ReduceOp.MAX)
+
+    def _exchange_staged(self):
+        """_exchange through host memory (gloo): same pairing and order."""
+        dist = self._dist
+        self.torch_stream.synchronize()
+        cpu = {k: (t.cpu() if t is not None else None)
+               for k, t in (("sn", self._send_n), ("ss", self._send_s))}
+        rs = self._recv_s.cpu() if self._recv_s is not None else None
+        rn = self._recv_n.cpu() if self._recv_n is not None else None
+        ops = []
+        if self.north is not None:
+            ops.append(dist.P2POp(dist.isend, cpu["sn"], self.north))
+        if self.south is not None:
+            ops.append(dist.P2POp(dist.irecv, rs, self.south))
+        if self.south is not None:
+            ops.append(dist.P2POp(dist.isend, cpu["ss"], self.south))
+        if self.north is not None:
+            ops.append(dist.P2POp(dist.irecv, rn, self.north))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        slot = self._slot()
+        s = slot.cpu()
+        dist.all_reduce(s, op=dist.ReduceOp.MAX)
+        with self._ctx():
+            if rs is not None:
+                self._recv_s.copy_(rs)
+            if rn is not None:
+                self._recv_n.copy_(rn)
+            slot.copy_(s)
 
     def _ctx(self):
         if self.torch_stream is None:

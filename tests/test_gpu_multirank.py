@@ -1,0 +1,114 @@
+"""GPU, multi-process: the row-strip driver (StripRunner) with the real CUDA
+solver in every rank, on one B200.
+
+The round-end and SCALE runs use StripRunner over NCCL with one GPU per rank;
+a gpurun box has one GPU and NCCL refuses two ranks on one device, so these
+ranks talk over gloo (edge rows and the speed slot staged through host
+memory) while everything on the device side is the production path: the step
+kernels writing the send rows and the reduction slot, the ghost rows read
+from the receive buffers, the MAX-reduced slot driving the next launch's dt,
+snapshot pauses and the gather.  No kernel waits on another rank (all
+synchronisation is host-side), so sharing the GPU is safe.  The bar is the
+reference's layout contract (tests/test_parallel.cpp:215-238): STRICT strips
+equal the single-domain reference run bit for bit.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, normwise, problem_from_meta
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, out_dir, variant, partition):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0")
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    from conftest import problem_from_meta
+    from paper_1307_0491_b200.distributed import StripRunner, init_dist
+    m, init = case
+    p = problem_from_meta(m)
+    torch.cuda.set_device(0)
+    init_dist(world, backend="gloo")
+    runner = StripRunner(p, world, rank, device=0, variant=variant, partition=partition)
+    runner.upload_host(np.ascontiguousarray(init[runner.j0:runner.j0 + runner.nrows]))
+    runner.begin(max_steps=m["max_steps"], snapshots=m["snapshots"])
+    seen = []
+    st = runner.run(batch=4, on_snapshot=lambda t, f: seen.append(t))
+    field = runner.gather()
+    if rank == 0:
+        np.save(os.path.join(out_dir, "field.npy"), field)
+        np.save(os.path.join(out_dir, "meta.npy"), np.array([st.t, st.steps] + seen))
+    runner.close()
+    runner.shutdown()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["rand48x32", "bc_periodic", "bc_inflow_wall"])
+def test_strip_runner_ranks_on_one_gpu(tmp_path, golden, world, case):
+    import torch.multiprocessing as mp
+    from paper_1307_0491_b200 import abi
+    data, meta = golden
+    m = meta["cases"][case]
+    init = data[f"{case}_init"]
+    for variant, part in ((abi.VARIANT_STRICT, None), (abi.VARIANT_FAST, None)):
+        out = tmp_path / f"v{variant}"
+        out.mkdir()
+        mp.spawn(_worker, args=(world, _free_port(), (m, init), str(out), variant, part),
+                 nprocs=world, join=True)
+        field = np.load(out / "field.npy")
+        mt = np.load(out / "meta.npy")
+        assert mt[1] == m["steps"]
+        assert list(mt[2:]) == [s for s in m["snapshots"] if s <= m["t_final"]]
+        if variant == abi.VARIANT_STRICT:
+            assert mt[0] == m["t_final"]
+            assert np.array_equal(field, data[f"{case}_final"])
+        else:
+            assert np.all(normwise(field, data[f"{case}_final"]) <= 1e-9)
+
+
+def test_uneven_partition_on_one_gpu(tmp_path, golden):
+    """A work-balanced (uneven) partition through the same device path."""
+    import torch.multiprocessing as mp
+    from paper_1307_0491_b200 import abi
+    data, meta = golden
+    m = meta["cases"]["dune64_ag1"]
+    part = [(0, 13), (13, 40), (53, 11)]
+    mp.spawn(_worker, args=(3, _free_port(), (m, data["dune64_ag1_init"]), str(tmp_path),
+                            abi.VARIANT_STRICT, part), nprocs=3, join=True)
+    assert np.array_equal(np.load(tmp_path / "field.npy"), data["dune64_ag1_final"])
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's N > 1 path (torchrun, balanced strips with the measured
+    pilot refinement, max-over-ranks timing, e2e) end to end, two ranks
+    sharing the GPU over gloo: one valid JSON line from rank 0."""
+    import json
+    import subprocess
+    env = dict(os.environ, SILT_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "C3", "--steps", "3",
+           "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
+    assert d["config"]["parallelism"] == "row strips x2"
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
