@@ -415,7 +415,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     A.ctl = s->ctl;
     // rows per CTA: enough warps in flight for a fp64-latency-bound kernel
     const long long strips = (s->nx + kCellsPerWarp - 1) / kCellsPerWarp;
-    long long R = (strips * s->ny + 8191) / 8192;
+    long long R = (strips * s->ny + 16383) / 16384;  // C4s: 34, C4: 96 (capped), measured best
     R = std::max(4LL, std::min(96LL, R));  // 96: measured best for C4 and Q
     if (const char* e = std::getenv("SILT_ROWS")) R = std::max(1LL, std::atoll(e));
     if (problem->dim == 1) R = 1;

@@ -58,13 +58,14 @@ def main():
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ns", default="2,4,8", help="strip counts to measure")
     a = ap.parse_args()
     p = bench.build_global_problem(a.workload, 1)
     full = bench.device_initial_rows(a.workload, p, 0, p.ny, torch.device("cuda"))
     costs = row_costs(full)
     t1 = strip_ms(p, full, 0, p.ny, a.steps, a.warmup)
     out = {"workload": a.workload, "t1_ms": t1, "runs": []}
-    for n in (2, 4, 8):
+    for n in [int(x) for x in a.ns.split(",")]:
         bal = balanced_partition(costs, n)
         bal_t = [strip_ms(p, full, j0, c, 4, 3) for j0, c in bal]  # pilot 1
         ref1 = refine_partition(costs, bal, bal_t)
