@@ -239,6 +239,16 @@ int silt_solver_cfl_dt(silt_solver* s, double* dt);
  * stream order) before enqueueing that step. */
 int silt_solver_reduce_slot(silt_solver* s, double** dev_ptr);
 int silt_solver_exchange_ptrs(silt_solver* s, silt_exchange* out);
+/* Halo/compute overlap for multi-rank drivers: one step in two launches.
+ * Part 1 runs the two boundary row blocks of the strip (they read the
+ * received ghost rows and write the send rows), part 2 the interior blocks
+ * and ends the step.  After part 1 (e.g. an event on the solver's stream) a
+ * driver may move the edge rows to and from the neighbours while part 2
+ * runs; the speed slot is complete after part 2.  *ok = 0 when the strip does
+ * not split (1D, fewer than 3 row blocks, no neighbour, or a launch long
+ * enough to use the dynamic row-block order): use silt_solver_step. */
+int silt_solver_step_split_ok(silt_solver* s, int* ok);
+int silt_solver_step_part(silt_solver* s, int part);
 /* Number of kernel launches this handle has enqueued (for accounting). */
 int silt_solver_launch_count(silt_solver* s, int64_t* count);
 

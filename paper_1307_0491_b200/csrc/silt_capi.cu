@@ -162,6 +162,7 @@ struct silt_solver {
     void* rb_mem = nullptr;     // row-block order: default, lists, 3 tables, 3 hot flags
     int* rb_default = nullptr;
     int* rb_lists = nullptr;
+    int* split_map = nullptr;   // {0, nb-1, 1, 2, ..., nb-2}: edge and interior row blocks
     int row_blocks = 0;
     int rb_span = 900;          // hot row blocks spread over this share (per mille) of a launch
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
@@ -261,14 +262,26 @@ int check_cfl(double cfl) {
     return SILT_OK;
 }
 
-void launch_step(silt_solver* s) {
+// part 0: the whole step; 1: the two boundary row blocks of a split step;
+// 2: its interior row blocks (and the end of the step).
+void launch_step(silt_solver* s, int part = 0) {
     const int li = (int)(s->launches % 3);
+    StepArgs a = s->args;
+    dim3 grid = s->step_grid;
+    if (part == 0) {
+        a.rb_map = a.rb_order ? a.rb_table[li] : nullptr;
+    } else {
+        a.rb_map = part == 1 ? s->split_map : s->split_map + 2;
+        a.epilogue = part == 1 ? 1 : 0;
+        grid.y = part == 1 ? 2u : grid.y - 2u;
+    }
     if (s->variant == SILT_VARIANT_STRICT)
-        silt_strict_step(s->args, li, s->step_grid, s->stream);
+        silt_strict_step(a, li, grid, s->stream);
     else
-        silt_fast_step(s->args, li, s->step_grid, s->stream);
-    ++s->launches;
+        silt_fast_step(a, li, grid, s->stream);
     ++s->kernel_count;
+    if (part == 1) return;
+    ++s->launches;
     if (s->args.rb_order) {
         rb_order_kernel<<<1, 1024, 0, s->stream>>>(s->args.rb_hot[li], s->rb_default, s->rb_lists,
                                                    s->args.rb_table[(li + 1) % 3], s->row_blocks,
@@ -442,6 +455,15 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         const bool order = problem->dim == 2 && nb >= 16 && (e ? e[0] != '0' : ctas >= 64LL * sms);
         s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta), nb, 1);
         A.rb_order = order ? 1 : 0;
+        A.epilogue = 1;
+        A.rb_map = nullptr;
+        if (!order && problem->dim == 2 && nb >= 3 && (st.south_neighbor || st.north_neighbor)) {
+            std::vector<int> m{0, (int)nb - 1};
+            for (unsigned k = 1; k + 1 < nb; ++k) m.push_back((int)k);
+            if (cudaMalloc(&s->split_map, m.size() * sizeof(int)) != cudaSuccess)
+                return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: device allocation failed"));
+            cudaMemcpy(s->split_map, m.data(), m.size() * sizeof(int), cudaMemcpyHostToDevice);
+        }
         if (const char* es = std::getenv("SILT_RB_SPAN")) s->rb_span = std::max(100, std::min(1000, std::atoi(es)));
         s->row_blocks = (int)nb;
         if (order) {
@@ -481,6 +503,7 @@ int silt_solver_destroy(silt_solver* s) {
     if (s->cap_done) cudaEventDestroy(s->cap_done);
     cudaFree(s->snapbuf);
     cudaFree(s->rb_mem);
+    cudaFree(s->split_map);
     cudaFree(s->planes);
     cudaFree(s->rows);
     cudaFree(s->cols);
@@ -730,6 +753,25 @@ int silt_solver_step(silt_solver* s, int n) {
     if (int rc = check_cfl(s->prob.cfl)) return rc;
     CUDA_TRY(cudaSetDevice(s->device));
     for (int k = 0; k < n; ++k) launch_step(s);
+    CUDA_TRY(cudaGetLastError());
+    return SILT_OK;
+}
+
+int silt_solver_step_split_ok(silt_solver* s, int* ok) {
+    if (!s || !ok) return fail(SILT_ERR_INVALID, "silt_solver_step_split_ok: null argument");
+    *ok = s->split_map != nullptr;
+    return SILT_OK;
+}
+
+int silt_solver_step_part(silt_solver* s, int part) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_step_part: call silt_solver_begin first");
+    if (part != 1 && part != 2) return fail(SILT_ERR_INVALID, "silt_solver_step_part: part is 1 or 2");
+    if (!s->split_map)
+        return fail(SILT_ERR_UNSUPPORTED, "silt_solver_step_part: this strip does not split");
+    if (int rc = check_cfl(s->prob.cfl)) return rc;
+    CUDA_TRY(cudaSetDevice(s->device));
+    launch_step(s, part);
     CUDA_TRY(cudaGetLastError());
     return SILT_OK;
 }

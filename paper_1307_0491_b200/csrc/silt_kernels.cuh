@@ -540,7 +540,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
 
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) control_epilogue(A, li, cur, d);
+    if (A.epilogue && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        control_epilogue(A, li, cur, d);
     if (!d.run) return;
     Slot& nxt = A.ctl->slot[(li + 1) % 3];
 
@@ -553,8 +554,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const int col = i0 - 1 + lane;
     const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < A.nx;
     const bool xface = lane <= kCellsPerWarp && col <= A.nx - 1;  // face at right of col
-    const int jb = (A.rb_order ? __ldg(A.rb_table[li] + blockIdx.y) : (int)blockIdx.y) *
-                   A.rows_per_block;
+    const int jb = (A.rb_map ? __ldg(A.rb_map + blockIdx.y) : (int)blockIdx.y) * A.rows_per_block;
     const int je = min(jb + A.rows_per_block, A.ny);
     if (jb >= je) return;
     if (lane == 0) sm.nfull[t >> 5] = 0;
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         __syncwarp();
     }
     if (A.rb_order && lane == 0 && sm.nfull[t >> 5] > kHotRows)
-        A.rb_hot[li][__ldg(A.rb_table[li] + blockIdx.y)] = 1;
+        A.rb_hot[li][__ldg(A.rb_map + blockIdx.y)] = 1;
     reduce_flush(R, nxt);
 }
 

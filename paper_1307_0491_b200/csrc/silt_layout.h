@@ -69,6 +69,11 @@ struct StepArgs {
     int rb_order;
     int* rb_table[3];
     unsigned char* rb_hot[3];
+    // Per launch: row block of blockIdx.y (nullptr: identity), and whether
+    // this launch runs the run-clock epilogue (the interior launch of a
+    // split step does not: the edge launch of the same step did).
+    const int* rb_map;
+    int epilogue;
     double dx, dy, cfl;
     silt_dev::Params P;
     int bc_type[4];

@@ -209,6 +209,13 @@ class StripRunner:
             # memory (used by the one-GPU multi-process tests; NCCL moves the
             # device buffers directly)
             self._stage = self.torch_stream is not None and dist.get_backend() == "gloo"
+        # halo/compute overlap (silt_solver_step_part); SILT_OVERLAP=0 disables
+        self._overlap = (world > 1 and self.torch_stream is not None and
+                         os.environ.get("SILT_OVERLAP", "1") != "0" and self.solver.split_ok())
+        if self._overlap and not self._stage:
+            import torch
+            self._comm = torch.cuda.Stream(device=self.device)
+            self._ev = torch.cuda.Event()
 
     def _wrap(self, ptr, n):
         if not ptr:
@@ -223,58 +230,81 @@ class StripRunner:
         return torch.as_tensor(_CAI(self.solver.reduce_slot(), 2), device=self.device)
 
     # ---- exchange ---------------------------------------------------------
-    def _exchange(self):
-        """Ghost rows of the newest state to the neighbours, then MAX of the
-        axis speeds.  Order per rank: send north, recv south, send south, recv
-        north — consistent pairing also when south == north (periodic, G=2)."""
-        if self.world == 1:
-            return
-        if self._stage:
-            return self._exchange_staged()
+    def _row_ops(self, send_n, recv_s, send_s, recv_n):
+        """Order per rank: send north, recv south, send south, recv north —
+        consistent pairing also when south == north (periodic, G = 2)."""
         dist = self._dist
         ops = []
         if self.north is not None:
-            ops.append(dist.P2POp(dist.isend, self._send_n, self.north))
+            ops.append(dist.P2POp(dist.isend, send_n, self.north))
         if self.south is not None:
-            ops.append(dist.P2POp(dist.irecv, self._recv_s, self.south))
+            ops.append(dist.P2POp(dist.irecv, recv_s, self.south))
         if self.south is not None:
-            ops.append(dist.P2POp(dist.isend, self._send_s, self.south))
+            ops.append(dist.P2POp(dist.isend, send_s, self.south))
         if self.north is not None:
-            ops.append(dist.P2POp(dist.irecv, self._recv_n, self.north))
+            ops.append(dist.P2POp(dist.irecv, recv_n, self.north))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        dist.all_reduce(self._slot(), op=dist.ReduceOp.MAX)
 
-    def _exchange_staged(self):
-        """_exchange through host memory (gloo): same pairing and order."""
-        dist = self._dist
+    def _exchange_rows(self):
+        """Edge rows of the newest state to the neighbours' ghost rows."""
+        if not self._stage:
+            self._row_ops(self._send_n, self._recv_s, self._send_s, self._recv_n)
+            return
+        # gloo moves host tensors: stage the device rows
         self.torch_stream.synchronize()
-        cpu = {k: (t.cpu() if t is not None else None)
-               for k, t in (("sn", self._send_n), ("ss", self._send_s))}
+        sn = self._send_n.cpu() if self._send_n is not None else None
+        ss = self._send_s.cpu() if self._send_s is not None else None
         rs = self._recv_s.cpu() if self._recv_s is not None else None
         rn = self._recv_n.cpu() if self._recv_n is not None else None
-        ops = []
-        if self.north is not None:
-            ops.append(dist.P2POp(dist.isend, cpu["sn"], self.north))
-        if self.south is not None:
-            ops.append(dist.P2POp(dist.irecv, rs, self.south))
-        if self.south is not None:
-            ops.append(dist.P2POp(dist.isend, cpu["ss"], self.south))
-        if self.north is not None:
-            ops.append(dist.P2POp(dist.irecv, rn, self.north))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        slot = self._slot()
-        s = slot.cpu()
-        dist.all_reduce(s, op=dist.ReduceOp.MAX)
+        self._row_ops(sn, rs, ss, rn)
         with self._ctx():
             if rs is not None:
                 self._recv_s.copy_(rs)
             if rn is not None:
                 self._recv_n.copy_(rn)
+
+    def _reduce_slot(self):
+        """MAX of the axis speeds over all ranks (global_dt, src/parallel.cpp:200-206)."""
+        dist = self._dist
+        slot = self._slot()
+        if not self._stage:
+            dist.all_reduce(slot, op=dist.ReduceOp.MAX)
+            return
+        self.torch_stream.synchronize()
+        s = slot.cpu()
+        dist.all_reduce(s, op=dist.ReduceOp.MAX)
+        with self._ctx():
             slot.copy_(s)
+
+    def _exchange(self):
+        """Ghost rows of the newest state to the neighbours, then MAX of the
+        axis speeds."""
+        if self.world == 1:
+            return
+        self._exchange_rows()
+        self._reduce_slot()
+
+    def _step_overlapped(self):
+        """One step with the edge-row exchange overlapping the interior: the
+        boundary row blocks first (they read the received rows and write the
+        send rows), the exchange on a side stream after them, the interior
+        blocks meanwhile on the solver's stream, then the MAX all-reduce."""
+        import torch
+        self.solver.step_part(1)
+        if self._stage:  # gloo: host-staged, no concurrency, same device work
+            self._exchange_rows()
+            self.solver.step_part(2)
+            self._reduce_slot()
+            return
+        self._ev.record(self.torch_stream)
+        with torch.cuda.stream(self._comm):
+            self._comm.wait_event(self._ev)
+            self._row_ops(self._send_n, self._recv_s, self._send_s, self._recv_n)
+        self.solver.step_part(2)
+        self.torch_stream.wait_stream(self._comm)
+        self._reduce_slot()
 
     def _ctx(self):
         if self.torch_stream is None:
@@ -324,8 +354,11 @@ class StripRunner:
                 self.solver.step(n)
                 return
             for _ in range(n):
-                self.solver.step(1)
-                self._exchange()
+                if self._overlap:
+                    self._step_overlapped()
+                else:
+                    self.solver.step(1)
+                    self._exchange()
 
     def status(self):
         return self.solver.status()

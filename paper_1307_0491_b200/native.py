@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
         "silt_solver_capture_query": ([_VP, C.POINTER(C.c_int)], C.c_int),
         "silt_host_alloc": ([C.c_int64, C.POINTER(_VP)], C.c_int),
         "silt_host_free": ([_VP], C.c_int),
+        "silt_solver_step_split_ok": ([_VP, C.POINTER(C.c_int)], C.c_int),
+        "silt_solver_step_part": ([_VP, C.c_int], C.c_int),
         "silt_snapshot_to_string": ([_P, _VP, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                      C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
         "silt_write_snapshot": ([_P, _VP, C.c_int64, C.c_int64, C.c_double, C.c_char_p,
@@ -273,6 +275,15 @@ class Solver:
 
     def step(self, n: int = 1):
         check(self.L.silt_solver_step(self.h, int(n)))
+
+    def split_ok(self) -> bool:
+        ok = C.c_int(0)
+        check(self.L.silt_solver_step_split_ok(self.h, C.byref(ok)))
+        return bool(ok.value)
+
+    def step_part(self, part: int):
+        """Part 1 (boundary row blocks) or 2 (interior, ends the step) of a split step."""
+        check(self.L.silt_solver_step_part(self.h, int(part)))
 
     def step_fixed(self, dt: float):
         check(self.L.silt_solver_step_fixed(self.h, float(dt)))
