@@ -126,8 +126,6 @@ def main():
                 entry = {"dram_bytes_per_launch": b, "cells": a.cells,
                          "source": os.path.basename(a.out) + "_full.md"}
                 tj[a.workload] = entry
-                if a.workload == "C4s":  # the bench's C4 line scales this capture per cell
-                    tj["C4"] = dict(entry, note="per-cell bytes of the C4s capture scaled to C4")
                 json.dump(tj, open(tp, "w"), indent=1)
 
 
