@@ -165,6 +165,7 @@ struct silt_solver {
     int* split_map = nullptr;   // {0, nb-1, 1, 2, ..., nb-2}: edge and interior row blocks
     int row_blocks = 0;
     int rb_span = 900;          // hot row blocks spread over this share (per mille) of a launch
+    int coop_blocks = -1;       // 1D: co-resident CTAs of the cooperative step kernel (-1: unknown)
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
     cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
     bool cap_pending = false;
@@ -752,6 +753,28 @@ int silt_solver_step(silt_solver* s, int n) {
     if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_step: call silt_solver_begin first");
     if (int rc = check_cfl(s->prob.cfl)) return rc;
     CUDA_TRY(cudaSetDevice(s->device));
+    // 1D: n steps in one cooperative launch when the grid fits co-resident
+    // (step1d_coop_kernel); SILT_COOP=0 keeps one launch per step
+    static const bool coop = [] {
+        const char* e = std::getenv("SILT_COOP");
+        return !(e && e[0] == '0');
+    }();
+    if (coop && s->prob.dim == 1 && n > 1) {
+        if (s->coop_blocks < 0)
+            s->coop_blocks = s->variant == SILT_VARIANT_STRICT
+                                 ? silt_strict_step1d_coop_blocks(s->args.P.shields)
+                                 : silt_fast_step1d_coop_blocks(s->args.P.shields);
+        if ((int)s->step_grid.x <= s->coop_blocks) {
+            const int li0 = (int)(s->launches % 3);
+            const int rc = s->variant == SILT_VARIANT_STRICT
+                               ? silt_strict_step1d_coop(s->args, li0, n, s->step_grid, s->stream)
+                               : silt_fast_step1d_coop(s->args, li0, n, s->step_grid, s->stream);
+            if (rc != 0) return fail(SILT_ERR_CUDA, cudaGetErrorString((cudaError_t)rc));
+            s->launches += n;
+            ++s->kernel_count;
+            return SILT_OK;
+        }
+    }
     for (int k = 0; k < n; ++k) launch_step(s);
     CUDA_TRY(cudaGetLastError());
     return SILT_OK;

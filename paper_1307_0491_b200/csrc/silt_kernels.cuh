@@ -21,6 +21,8 @@
 // the clipping rule of run_serial (src/parallel.cpp:221-237), so a batch of
 // steps needs no host round trip.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "silt_layout.h"
 #include "silt_physics.cuh"
 
@@ -716,7 +718,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
 
 // ---- K2: 1D step (step_1d, src/stepper.cpp:118-140) ----------------------
 template <bool S, bool SH>
-__global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li) {
+__device__ __forceinline__ void step1d_body(const StepArgs& A, int li) {
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
     if (blockIdx.x == 0 && threadIdx.x == 0) control_epilogue(A, li, cur, d);
@@ -764,6 +766,28 @@ __global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li
         reduce_fold(A, R, o, ssx, ssy);
     }
     reduce_flush(R, nxt);
+}
+
+template <bool S, bool SH>
+__global__ void __launch_bounds__(kStepThreads) step1d_kernel(StepArgs A, int li) {
+    step1d_body<S, SH>(A, li);
+}
+
+// ---- K2c: n 1D steps in one cooperative launch --------------------------------
+// The 1D configurations are latency-bound (a few thousand cells: one face
+// solve per lane, then the global reduction); a launch per step adds the
+// launch and a cold start each time.  Here all CTAs stay resident and step n
+// times, a grid-wide barrier between steps (it orders the state writes and
+// the slot reductions of step k before step k+1 reads them).  Steps after the
+// run stopped (done / paused / failed) only propagate the run clock, exactly
+// as the per-step launches would, so launch index n keeps its meaning.
+template <bool S, bool SH>
+__global__ void __launch_bounds__(kStepThreads) step1d_coop_kernel(StepArgs A, int li0, int n) {
+    cooperative_groups::grid_group g = cooperative_groups::this_grid();
+    for (int k = 0; k < n; ++k) {
+        step1d_body<S, SH>(A, (li0 + k) % 3);
+        g.sync();
+    }
 }
 
 // ---- initial reduction of a state (first cfl_dt + hmax + ghost rows) --------
@@ -866,6 +890,23 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
             NAME##_step_t<true>(A, li, grid, st);                                                \
         else                                                                                     \
             NAME##_step_t<false>(A, li, grid, st);                                               \
+    }                                                                                            \
+    int NAME##_step1d_coop(const StepArgs& A, int li0, int n, dim3 grid, cudaStream_t st) {      \
+        StepArgs a = A;                                                                          \
+        void* args[] = {&a, &li0, &n};                                                           \
+        const void* f = A.P.shields ? (const void*)silt_dev::step1d_coop_kernel<S, true>         \
+                                    : (const void*)silt_dev::step1d_coop_kernel<S, false>;       \
+        return (int)cudaLaunchCooperativeKernel(f, grid, dim3(kStepThreads), args, 0, st);       \
+    }                                                                                            \
+    int NAME##_step1d_coop_blocks(int shields) {                                                 \
+        int per_sm = 0, sms = 0, dev = 0;                                                        \
+        cudaGetDevice(&dev);                                                                     \
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                       \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                           \
+            &per_sm,                                                                             \
+            shields ? silt_dev::step1d_coop_kernel<S, true> : silt_dev::step1d_coop_kernel<S, false>, \
+            kStepThreads, 0);                                                                    \
+        return per_sm * sms;                                                                     \
     }                                                                                            \
     void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st) {                 \
         if (A.P.shields)                                                                         \

@@ -6,6 +6,8 @@
 
 #define SILT_DECLARE_LAUNCHERS(NAME)                                                         \
     void NAME##_step(const StepArgs& A, int li, dim3 grid, cudaStream_t st);                 \
+    int NAME##_step1d_coop(const StepArgs& A, int li0, int n, dim3 grid, cudaStream_t st);   \
+    int NAME##_step1d_coop_blocks(int shields);                                              \
     void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st);              \
     void NAME##_faces(const silt_dev::Params& P, const double* L, const double* R,           \
                       long long n, int axis, double* out, unsigned* err, cudaStream_t st);   \
