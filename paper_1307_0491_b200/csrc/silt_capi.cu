@@ -1049,6 +1049,20 @@ int silt_group_create(const silt_problem* problem, int py, const int* devices, i
         g->stepped.push_back(e1);
         g->copied.push_back(e2);
     }
+    // direct NVLink copies between the devices in use (ghost rows, slots)
+    {
+        const int nd = std::min(n_devices, py);
+        for (int a = 0; a < nd; ++a)
+            for (int b = 0; b < nd; ++b) {
+                if (devices[a] == devices[b]) continue;
+                int ok = 0;
+                if (cudaDeviceCanAccessPeer(&ok, devices[a], devices[b]) == cudaSuccess && ok) {
+                    cudaSetDevice(devices[a]);
+                    if (cudaDeviceEnablePeerAccess(devices[b], 0) != cudaSuccess)
+                        cudaGetLastError();  // already enabled is fine
+                }
+            }
+    }
     cudaSetDevice(g->dev0);
     if (cudaStreamCreateWithFlags(&g->s0, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&g->reduced, cudaEventDisableTiming) != cudaSuccess ||

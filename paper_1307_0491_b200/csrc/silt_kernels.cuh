@@ -873,12 +873,15 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
     template <bool SH>                                                                           \
     static void NAME##_step_t(const StepArgs& A, int li, dim3 grid, cudaStream_t st) {           \
         if (A.dim == 2) {                                                                        \
-            static bool attr_set = false;                                                        \
-            if (!attr_set) {                                                                     \
+            /* the attribute is per device: one bit per device ordinal */                       \
+            static unsigned long long attr_set = 0;                                              \
+            int dev_ = 0;                                                                        \
+            cudaGetDevice(&dev_);                                                                \
+            if (!(attr_set >> (dev_ & 63) & 1ull)) {                                             \
                 cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH>,                             \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,                \
                                      (int)sizeof(silt_dev::StepSmem));                           \
-                attr_set = true;                                                                 \
+                attr_set |= 1ull << (dev_ & 63);                                                 \
             }                                                                                    \
             silt_dev::step2d_kernel<S, SH>                                                       \
                 <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);                 \
