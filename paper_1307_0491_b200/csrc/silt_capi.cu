@@ -166,6 +166,7 @@ struct silt_solver {
     int row_blocks = 0;
     int rb_span = 900;          // hot row blocks spread over this share (per mille) of a launch
     int coop_blocks = -1;       // 1D: co-resident CTAs of the cooperative step kernel (-1: unknown)
+    bool cluster_failed = false;  // 1D: the cluster launch was refused once
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
     cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
     bool cap_pending = false;
@@ -760,6 +761,28 @@ int silt_solver_step(silt_solver* s, int n) {
         return !(e && e[0] == '0');
     }();
     if (coop && s->prob.dim == 1 && n > 1) {
+        // one cluster (<= 16 CTAs of 384 threads) when the line fits, else a
+        // cooperative grid; SILT_COOP=2 forces the cooperative grid
+        const long long strips = (s->nx + kCellsPerWarp - 1) / kCellsPerWarp;
+        const int per_cta = 384 / 32;
+        const int ctas = (int)((strips + per_cta - 1) / per_cta);
+        static const bool cluster_ok = [] {
+            const char* e = std::getenv("SILT_COOP");
+            return !(e && e[0] == '2');
+        }();
+        if (cluster_ok && ctas <= 16 && !s->cluster_failed) {
+            const int li0 = (int)(s->launches % 3);
+            const int rc = s->variant == SILT_VARIANT_STRICT
+                               ? silt_strict_step1d_cluster(s->args, li0, n, ctas, s->stream)
+                               : silt_fast_step1d_cluster(s->args, li0, n, ctas, s->stream);
+            if (rc == 0) {
+                s->launches += n;
+                ++s->kernel_count;
+                return SILT_OK;
+            }
+            cudaGetLastError();  // cluster not schedulable here: fall back for good
+            s->cluster_failed = true;
+        }
         if (s->coop_blocks < 0)
             s->coop_blocks = s->variant == SILT_VARIANT_STRICT
                                  ? silt_strict_step1d_coop_blocks(s->args.P.shields)

@@ -726,7 +726,7 @@ __device__ __forceinline__ void step1d_body(const StepArgs& A, int li) {
     Slot& nxt = A.ctl->slot[(li + 1) % 3];
     const int p = (int)(cur.steps & 1), q = p ^ 1;
     const int lane = threadIdx.x & 31;
-    const int strip = blockIdx.x * (kStepThreads / 32) + (threadIdx.x >> 5);
+    const int strip = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int i0 = strip * kCellsPerWarp;
     if (i0 >= A.nx) return;
     const int col = i0 - 1 + lane;
@@ -787,6 +787,21 @@ __global__ void __launch_bounds__(kStepThreads) step1d_coop_kernel(StepArgs A, i
     for (int k = 0; k < n; ++k) {
         step1d_body<S, SH>(A, (li0 + k) % 3);
         g.sync();
+    }
+}
+
+// The same loop for grids that fit one thread-block cluster (up to 16 CTAs of
+// 384 threads: 5760 cells, C1 and C2): the per-step barrier is the cluster's
+// hardware barrier (release / acquire at cluster scope orders the state and
+// slot writes) instead of the grid-wide software barrier.
+constexpr int kCluster1dThreads = 384;
+template <bool S, bool SH>
+__global__ void __launch_bounds__(kCluster1dThreads, 1)
+    step1d_cluster_kernel(StepArgs A, int li0, int n) {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    for (int k = 0; k < n; ++k) {
+        step1d_body<S, SH>(A, (li0 + k) % 3);
+        cl.sync();
     }
 }
 
@@ -900,6 +915,25 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
         const void* f = A.P.shields ? (const void*)silt_dev::step1d_coop_kernel<S, true>         \
                                     : (const void*)silt_dev::step1d_coop_kernel<S, false>;       \
         return (int)cudaLaunchCooperativeKernel(f, grid, dim3(kStepThreads), args, 0, st);       \
+    }                                                                                            \
+    int NAME##_step1d_cluster(const StepArgs& A, int li0, int n, int ctas, cudaStream_t st) {    \
+        StepArgs a = A;                                                                          \
+        void* args[] = {&a, &li0, &n};                                                           \
+        const void* f = A.P.shields ? (const void*)silt_dev::step1d_cluster_kernel<S, true>      \
+                                    : (const void*)silt_dev::step1d_cluster_kernel<S, false>;    \
+        cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);              \
+        cudaLaunchConfig_t cfg{};                                                                \
+        cfg.gridDim = dim3(ctas);                                                                \
+        cfg.blockDim = dim3(silt_dev::kCluster1dThreads);                                        \
+        cfg.stream = st;                                                                         \
+        cudaLaunchAttribute at[1];                                                               \
+        at[0].id = cudaLaunchAttributeClusterDimension;                                          \
+        at[0].val.clusterDim.x = ctas;                                                           \
+        at[0].val.clusterDim.y = 1;                                                              \
+        at[0].val.clusterDim.z = 1;                                                              \
+        cfg.attrs = at;                                                                          \
+        cfg.numAttrs = 1;                                                                        \
+        return (int)cudaLaunchKernelExC(&cfg, f, args);                                          \
     }                                                                                            \
     int NAME##_step1d_coop_blocks(int shields) {                                                 \
         int per_sm = 0, sms = 0, dev = 0;                                                        \
