@@ -227,6 +227,11 @@ int silt_solver_resume(silt_solver* s);
 int silt_solver_capture_resume(silt_solver* s, double* host_aos);
 int silt_solver_capture_wait(silt_solver* s);
 int silt_solver_capture_query(silt_solver* s, int* landed);
+/* write_snapshot of a paused solver without holding the run: the state is
+ * copied on the device, the solver resumes, and a host thread formats the
+ * copy on the device and writes `path` (header unless `append`) while the
+ * next steps run.  silt_solver_capture_wait joins it and reports its error. */
+int silt_solver_capture_write(silt_solver* s, double time, const char* path, int append);
 /* Page-locked host memory (capture targets, fast uploads). */
 int silt_host_alloc(int64_t bytes, void** out);
 int silt_host_free(void* p);

@@ -18,6 +18,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "silt_csv_launch.h"
 #include "silt_cuda.h"
@@ -170,6 +171,9 @@ struct silt_solver {
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
     cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
     bool cap_pending = false;
+    std::thread writer;         // asynchronous CSV snapshot (silt_solver_capture_write)
+    int writer_rc = SILT_OK;
+    std::string writer_err;
     Control* ctl = nullptr;
     Control* host_ctl = nullptr;  // pinned staging for control uploads
     double* dt_log = nullptr;
@@ -495,6 +499,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
 
 int silt_solver_destroy(silt_solver* s) {
     if (!s) return SILT_OK;
+    if (s->writer.joinable()) s->writer.join();
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->copy_stream) {
@@ -596,6 +601,15 @@ int silt_solver_download_device(silt_solver* s, double* dev_aos) {
 
 int silt_solver_capture_wait(silt_solver* s) {
     if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    if (s->writer.joinable()) {  // an asynchronous CSV snapshot in flight
+        s->writer.join();
+        s->cap_pending = false;
+        if (s->writer_rc != SILT_OK) {
+            const int rc = s->writer_rc;
+            s->writer_rc = SILT_OK;
+            return fail(rc, s->writer_err);
+        }
+    }
     if (!s->cap_pending) return SILT_OK;
     CUDA_TRY(cudaSetDevice(s->device));
     CUDA_TRY(cudaEventSynchronize(s->cap_done));
@@ -1613,3 +1627,58 @@ int silt_group_write_snapshot(silt_group* g, double time, const char* path, int6
 }
 
 }  // extern "C"
+
+// ---- asynchronous CSV snapshot ---------------------------------------------------
+// write_snapshot of a paused run without holding it: the state is copied into
+// the snapshot buffer on the solver's stream, the run resumes, and a host
+// thread formats the buffer on the device (CSV stream, concurrent with the
+// next steps) and writes the file.  silt_solver_capture_wait joins it.
+extern "C" int silt_solver_capture_write(silt_solver* s, double time, const char* path,
+                                         int append) {
+    if (!s || !path) return fail(SILT_ERR_INVALID, "silt_solver_capture_write: null argument");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_capture_write: run not begun");
+    if (int rc = silt_solver_capture_wait(s)) return rc;
+    CUDA_TRY(cudaSetDevice(s->device));
+    const size_t bytes = 4 * (size_t)s->nx * s->ny * sizeof(double);
+    if (!s->snapbuf) {
+        CUDA_TRY(cudaMalloc(&s->snapbuf, bytes));
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->cap_ready, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->cap_done, cudaEventDisableTiming));
+    }
+    Slot sl;
+    if (int rc = read_slot(s, &sl, nullptr)) return rc;
+    if (sl.state != SILT_STATE_PAUSED)
+        return fail(SILT_ERR_INVALID, "silt_solver_capture_write: solver is not paused");
+    const int p = (int)(sl.steps & 1);
+    const StepArgs& A = s->args;
+    soa_to_aos<<<grid_blocks((long long)s->nx * s->ny, 256), 256, 0, s->stream>>>(
+        s->snapbuf, A.state[p][0], A.state[p][1], A.state[p][2], A.state[p][3], s->nx, s->ny,
+        s->pitch);
+    ++s->kernel_count;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(s->cap_ready, s->stream));
+    int st = SILT_STATE_RUNNING;
+    Slot* slot = &s->ctl->slot[s->launches % 3];
+    CUDA_TRY(cudaMemcpy(&slot->state, &st, sizeof(int), cudaMemcpyHostToDevice));
+    const std::string file(path);
+    s->writer_rc = SILT_OK;
+    s->writer = std::thread([s, time, file, append] {
+        cudaSetDevice(s->device);
+        if (cudaEventSynchronize(s->cap_ready) != cudaSuccess) {
+            s->writer_rc = SILT_ERR_CUDA;
+            s->writer_err = "silt_solver_capture_write: capture failed";
+            return;
+        }
+        CsvSink sink;
+        int rc = open_sink(sink, file.c_str(), append != 0);
+        if (rc == SILT_OK) {
+            rc = csv_emit(s->device, aos_field(s->snapbuf, s->nx), nullptr, s->prob, s->ny,
+                          s->strip.j0, time, append == 0, sink);
+            rc = close_sink(sink, rc);
+        }
+        s->writer_rc = rc;
+        if (rc != SILT_OK) s->writer_err = silt_last_error();
+    });
+    return SILT_OK;
+}

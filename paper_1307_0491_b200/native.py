@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         "silt_solver_capture_resume": ([_VP, _D], C.c_int),
         "silt_solver_capture_wait": ([_VP], C.c_int),
         "silt_solver_capture_query": ([_VP, C.POINTER(C.c_int)], C.c_int),
+        "silt_solver_capture_write": ([_VP, C.c_double, C.c_char_p, C.c_int], C.c_int),
         "silt_host_alloc": ([C.c_int64, C.POINTER(_VP)], C.c_int),
         "silt_host_free": ([_VP], C.c_int),
         "silt_solver_step_split_ok": ([_VP, C.POINTER(C.c_int)], C.c_int),
@@ -329,6 +330,29 @@ class Solver:
 
     def capture_wait(self):
         check(self.L.silt_solver_capture_wait(self.h))
+
+    def capture_write(self, time: float, path: str, append: bool = False):
+        """CSV snapshot of a paused run, written in the background while the run
+        continues (silt_solver_capture_write); capture_wait() joins it."""
+        check(self.L.silt_solver_capture_write(self.h, float(time), os.fsencode(path),
+                                               int(append)))
+
+    def run_csv(self, pattern: str, batch: int = 32) -> SiltStatus:
+        """Advance until DONE, writing every snapshot as CSV (pattern % index,
+        e.g. 'out/snap_%04d.csv') in the background."""
+        k = 0
+        try:
+            while True:
+                self.step(batch)
+                st = self.status()
+                if st.state == abi.STATE_PAUSED:
+                    self.capture_write(st.t, pattern % k)
+                    k += 1
+                    continue
+                if st.state == abi.STATE_DONE:
+                    return st
+        finally:
+            self.capture_wait()
 
     def write_snapshot(self, time: float, path: str, append: bool = False) -> int:
         """CSV of the current state (write_snapshot) formatted on the device."""

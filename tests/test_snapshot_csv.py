@@ -181,3 +181,31 @@ def test_gpu_csv_chunks_solver_and_group(N, restatement, golden, tmp_path, monke
     g.write_snapshot(st.t, path)
     g.close()
     assert open(path, "rb").read() == want
+
+
+@pytest.mark.gpu
+def test_gpu_async_csv_snapshots(N, restatement, golden, tmp_path):
+    """silt_solver_capture_write: every snapshot of a run written as CSV in the
+    background while the run continues; each file equals the restatement's CSV
+    of the reference path run to that time (STRICT), and the run's end state
+    is unaffected."""
+    data, meta = golden
+    m = meta["cases"]["rand48x32"]
+    p = problem_from_meta(m)
+    init = data["rand48x32_init"]
+    T = m["t_final"]
+    snaps = [0.2 * T, 0.2 * T + 1e-9, 0.6 * T]
+    s = N.Solver(p, variant=abi.VARIANT_STRICT)
+    s.upload(init)
+    s.begin(max_steps=m["max_steps"] + len(snaps), snapshots=snaps)
+    st = s.run_csv(str(tmp_path / "snap_%02d.csv"), batch=5)
+    final = s.download()
+    s.close()
+    for k, t in enumerate(snaps):
+        ref, rt, _, _ = restatement.run(p, init, t_end=t, snapshots=[x for x in snaps if x < t])
+        assert rt == t
+        want = restatement.snapshot_to_string(p, ref, t)
+        assert open(tmp_path / f"snap_{k:02d}.csv", "rb").read() == want, k
+    ref, rt, n, _ = restatement.run(p, init, max_steps=m["max_steps"] + len(snaps),
+                                    snapshots=snaps)
+    assert st.steps == n and np.array_equal(final, ref)

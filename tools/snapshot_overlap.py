@@ -60,6 +60,29 @@ def main():
         out["async" if mode else "sync"] = {"wall_s": wall, "steps": st.steps, "sum_h": sums}
     out["saved_s"] = out["sync"]["wall_s"] - out["async"]["wall_s"]
     assert out["sync"]["sum_h"] == out["async"]["sum_h"]
+    # CSV snapshots (device formatter) to /dev/null: between steps vs in the background
+    for mode in ("csv_sync", "csv_async"):
+        s = native.Solver(p)
+        s.upload_device(full.data_ptr())
+        s.write_snapshot(0.0, "/dev/null")  # CSV context warm-up
+        s.begin(max_steps=a.steps + a.snaps, snapshots=snaps)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if mode == "csv_async":
+            st = s.run_csv("/dev/null%.0s", batch=32)  # every snapshot to /dev/null
+        else:
+            while True:
+                s.step(32)
+                st = s.status()
+                if st.state == 2:
+                    s.write_snapshot(st.t, "/dev/null")
+                    s.resume()
+                    continue
+                if st.state == 1:
+                    break
+        torch.cuda.synchronize()
+        out[mode] = {"wall_s": time.perf_counter() - t0, "steps": st.steps}
+        s.close()
     print(json.dumps(out))
 
 
