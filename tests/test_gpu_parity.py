@@ -392,3 +392,43 @@ def test_quiet_row_skip_is_bit_identical(N, golden, case, monkeypatch):
     assert outs[0][2] == outs[1][2] == steps
     assert np.array_equal(outs[0][3], outs[1][3])
     assert np.array_equal(outs[0][0], outs[1][0])
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (2, 2), (29, 3), (30, 2), (31, 2),
+                                   (61, 5), (90, 1), (121, 9)])
+def test_degenerate_shapes(N, restatement, shape):
+    """Grids at and around the warp band width (30 owned columns) and single
+    rows / columns, with every BC type: STRICT bitwise, FAST within the bar."""
+    nx, ny = shape
+    rng = np.random.default_rng(nx * 131 + ny)
+    init = np.empty((ny, nx, 4))
+    init[..., 3] = 0.1 + 0.05 * rng.random((ny, nx))
+    init[..., 0] = 1.5 - init[..., 3] + 0.05 * rng.random((ny, nx))
+    init[..., 1] = init[..., 0] * rng.uniform(0.2, 0.8, (ny, nx))
+    init[..., 2] = init[..., 0] * rng.uniform(-0.2, 0.2, (ny, nx))
+    for bcs in ([abi.bc("outflow")] * 4,
+                [abi.bc("inflow", q0=0.7), abi.bc("wall"), abi.bc("periodic"), abi.bc("periodic")],
+                [abi.bc("periodic"), abi.bc("periodic"), abi.bc("wall"), abi.bc("outflow")]):
+        p = abi.make_problem(2, nx, ny, 1.0, 1.0, a_g=0.3, bcs=bcs)
+        ref, t, n, log = restatement.run(p, init, max_steps=12)
+        so, st, sn, slog = N.run(p, init, max_steps=12, variant=abi.VARIANT_STRICT)
+        assert sn == n and st == t and np.array_equal(so, ref) and np.array_equal(slog, log)
+        fo, ft, fn, flog = N.run(p, init, max_steps=12, variant=abi.VARIANT_FAST)
+        assert fn == n and np.all(normwise(fo, ref) <= FIELD_TOL)
+
+
+@pytest.mark.parametrize("nx", [1, 2, 29, 30, 31, 61, 359, 360, 361, 5761])
+def test_degenerate_1d(N, restatement, nx):
+    """1D lines around the warp (30), cluster-CTA (360) and cluster (5760)
+    widths: single launches, cluster launches and the cooperative fallback."""
+    rng = np.random.default_rng(nx)
+    init = np.zeros((1, nx, 4))
+    init[0, :, 3] = 0.1 + 0.05 * rng.random(nx)
+    init[0, :, 0] = 1.5 - init[0, :, 3]
+    init[0, :, 1] = 0.6 * init[0, :, 0]
+    for bcs in ([abi.bc("outflow")] * 4, [abi.bc("periodic"), abi.bc("periodic"),
+                                          abi.bc("outflow"), abi.bc("outflow")]):
+        p = abi.make_problem(1, nx, 1, 1.0, 1.0, a_g=0.3, bcs=bcs)
+        ref, t, n, log = restatement.run(p, init, max_steps=40)
+        so, st, sn, slog = N.run(p, init, max_steps=40, variant=abi.VARIANT_STRICT)
+        assert sn == n and st == t and np.array_equal(so, ref) and np.array_equal(slog, log)
