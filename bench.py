@@ -333,7 +333,9 @@ def main():
     value = cells * args.steps / (ms / 1e3)
     ms_step = ms / args.steps
     peak, peak_src = peaks()
-    per_gpu_cells = nrows * p.nx
+    # per-GPU average (strips may be uneven: work-balanced partition); the
+    # step time is the max over ranks
+    per_gpu_cells = cells / world
     achieved = per_gpu_cells * BYTES_PER_CELL / (ms_step / 1e3) / 1e9
     traffic = None
     try:
