@@ -383,13 +383,13 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         return cleanup(fail(SILT_ERR_CUDA, "cudaStreamCreate failed"));
     s->own_stream = true;
     if (cudaMalloc(&s->planes, 8 * plane * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&s->rows, 8 * 4 * (size_t)s->nx * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&s->rows, 10 * 4 * (size_t)s->nx * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&s->cols, 2 * 4 * (size_t)s->ny * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&s->ctl, sizeof(Control)) != cudaSuccess ||
         cudaMallocHost(&s->host_ctl, sizeof(Control)) != cudaSuccess)
         return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: device allocation failed"));
     cudaMemset(s->planes, 0, 8 * plane * sizeof(double));
-    cudaMemset(s->rows, 0, 8 * 4 * (size_t)s->nx * sizeof(double));
+    cudaMemset(s->rows, 0, 10 * 4 * (size_t)s->nx * sizeof(double));
     cudaMemset(s->cols, 0, 2 * 4 * (size_t)s->ny * sizeof(double));
     cudaMemset(s->ctl, 0, sizeof(Control));
 
@@ -425,10 +425,12 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     A.ghost_s[1] = s->rows + 1 * row;
     A.ghost_n[0] = s->rows + 2 * row;
     A.ghost_n[1] = s->rows + 3 * row;
-    A.recv_s = s->rows + 4 * row;
-    A.recv_n = s->rows + 5 * row;
-    A.send_s = s->rows + 6 * row;
-    A.send_n = s->rows + 7 * row;
+    // single-buffered exchange rows (rows 8, 9: the second recv parity of the
+    // group's direct mode)
+    A.recv_s[0] = A.recv_s[1] = s->rows + 4 * row;
+    A.recv_n[0] = A.recv_n[1] = s->rows + 5 * row;
+    A.send_s[0] = A.send_s[1] = s->rows + 6 * row;
+    A.send_n[0] = A.send_n[1] = s->rows + 7 * row;
     A.ghost_w = s->cols;
     A.ghost_e = s->cols + 4 * (size_t)s->ny;
     A.ctl = s->ctl;
@@ -924,10 +926,10 @@ int silt_solver_reduce_slot(silt_solver* s, double** dev_ptr) {
 
 int silt_solver_exchange_ptrs(silt_solver* s, silt_exchange* out) {
     if (!s || !out) return fail(SILT_ERR_INVALID, "silt_solver_exchange_ptrs: null argument");
-    out->send_south = s->strip.south_neighbor ? s->args.send_s : nullptr;
-    out->send_north = s->strip.north_neighbor ? s->args.send_n : nullptr;
-    out->recv_south = s->strip.south_neighbor ? s->args.recv_s : nullptr;
-    out->recv_north = s->strip.north_neighbor ? s->args.recv_n : nullptr;
+    out->send_south = s->strip.south_neighbor ? s->args.send_s[0] : nullptr;
+    out->send_north = s->strip.north_neighbor ? s->args.send_n[0] : nullptr;
+    out->recv_south = s->strip.south_neighbor ? s->args.recv_s[0] : nullptr;
+    out->recv_north = s->strip.north_neighbor ? s->args.recv_n[0] : nullptr;
     out->row_doubles = 4 * (int64_t)s->nx;
     return SILT_OK;
 }
@@ -942,6 +944,16 @@ int silt_solver_launch_count(silt_solver* s, int64_t* count) {
 
 // ---- strip group --------------------------------------------------------------
 namespace {
+
+// direct mode: this strip's maxima of the state just produced into every
+// other strip's slot (remote atomics over NVLink / same-device atomics)
+__global__ void push_max_kernel(const Control* local, int slot, Control* const* peers, int n) {
+    const unsigned long long sx = local->slot[slot].max_sx, sy = local->slot[slot].max_sy;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        atomicMax(&peers[k]->slot[slot].max_sx, sx);
+        atomicMax(&peers[k]->slot[slot].max_sy, sy);
+    }
+}
 
 __global__ void max_slots_kernel(const double* gathered, int n, double* result) {
     double sx = 0.0, sy = 0.0;
@@ -965,6 +977,14 @@ struct silt_group {
     std::vector<silt_solver*> strips;
     std::vector<int> south, north;   // neighbour strip or -1
     std::vector<cudaEvent_t> stepped, copied;
+    // direct mode: the step kernels store their edge rows into the
+    // neighbours' recv rows (peer memory) and push_max_kernel folds each
+    // strip's axis-speed maxima into every other strip's slot; per step the
+    // strips only wait on each other's events (no copies, no reduction stream)
+    bool direct = false;
+    std::vector<Control**> peers;    // per strip, on its device: the other strips' Control
+    std::vector<cudaEvent_t> pushed;
+    bool joined = false;             // `reduced` marks the last direct step of every strip
     int dev0 = 0;
     double* gathered = nullptr;      // on dev0: [py][2]
     double* result = nullptr;        // on dev0: [2]
@@ -995,6 +1015,7 @@ int group_exchange(silt_group* g) {
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(g->reduced, g->s0));
     // 3. per strip: reduced maxima + ghost rows from the neighbours' send rows
+    //    (direct mode: the rows are already in place)
     const size_t row = 4 * (size_t)g->nx * sizeof(double);
     for (int k = 0; k < py; ++k) {
         silt_solver* s = g->strips[k];
@@ -1003,17 +1024,21 @@ int group_exchange(silt_group* g) {
         Slot* slot = &s->ctl->slot[s->launches % 3];
         CUDA_TRY(cudaMemcpyAsync(&slot->max_sx, g->result, 2 * sizeof(double), cudaMemcpyDefault,
                                  s->stream));
+        if (g->direct) {
+            CUDA_TRY(cudaEventRecord(g->copied[k], s->stream));
+            continue;
+        }
         if (g->south[k] >= 0) {
             silt_solver* src = g->strips[g->south[k]];
             CUDA_TRY(cudaStreamWaitEvent(s->stream, g->stepped[g->south[k]], 0));
-            CUDA_TRY(cudaMemcpyAsync(s->args.recv_s, src->args.send_n, row, cudaMemcpyDefault,
-                                     s->stream));
+            CUDA_TRY(cudaMemcpyAsync(s->args.recv_s[0], src->args.send_n[0], row,
+                                     cudaMemcpyDefault, s->stream));
         }
         if (g->north[k] >= 0) {
             silt_solver* src = g->strips[g->north[k]];
             CUDA_TRY(cudaStreamWaitEvent(s->stream, g->stepped[g->north[k]], 0));
-            CUDA_TRY(cudaMemcpyAsync(s->args.recv_n, src->args.send_s, row, cudaMemcpyDefault,
-                                     s->stream));
+            CUDA_TRY(cudaMemcpyAsync(s->args.recv_n[0], src->args.send_s[0], row,
+                                     cudaMemcpyDefault, s->stream));
         }
         CUDA_TRY(cudaEventRecord(g->copied[k], s->stream));
     }
@@ -1033,6 +1058,12 @@ extern "C" {
 
 int silt_group_destroy(silt_group* g) {
     if (!g) return SILT_OK;
+    for (size_t k = 0; k < g->peers.size(); ++k) {
+        cudaSetDevice(g->strips[k]->device);
+        cudaStreamSynchronize(g->strips[k]->stream);
+        if (g->peers[k]) cudaFree(g->peers[k]);
+        if (g->pushed[k]) cudaEventDestroy(g->pushed[k]);
+    }
     for (silt_solver* s : g->strips) silt_solver_destroy(s);
     cudaSetDevice(g->dev0);
     if (g->s0) cudaStreamSynchronize(g->s0);
@@ -1100,6 +1131,50 @@ int silt_group_create(const silt_problem* problem, int py, const int* devices, i
                 }
             }
     }
+    // direct mode: every pair of strip devices can reach the other's memory
+    {
+        const char* e = std::getenv("SILT_GROUP_DIRECT");
+        bool ok = py > 1 && problem->dim == 2 && !(e && e[0] == '0');
+        for (int a = 0; ok && a < py; ++a)
+            for (int b = 0; ok && b < py; ++b) {
+                const int da = g->strips[a]->device, db = g->strips[b]->device;
+                int can = 1;
+                if (da != db && (cudaDeviceCanAccessPeer(&can, da, db) != cudaSuccess || !can))
+                    ok = false;
+            }
+        if (ok) {
+            const size_t row = 4 * (size_t)g->nx;
+            for (silt_solver* s : g->strips) {  // second parity of the receive rows
+                s->args.recv_s[1] = s->rows + 8 * row;
+                s->args.recv_n[1] = s->rows + 9 * row;
+            }
+            for (int k = 0; k < py; ++k) {
+                StepArgs& A = g->strips[k]->args;
+                for (int q = 0; q < 2; ++q) {
+                    if (g->south[k] >= 0) A.send_s[q] = g->strips[g->south[k]]->args.recv_n[q];
+                    if (g->north[k] >= 0) A.send_n[q] = g->strips[g->north[k]]->args.recv_s[q];
+                }
+            }
+            g->peers.assign(py, nullptr);
+            g->pushed.assign(py, nullptr);
+            for (int k = 0; k < py && ok; ++k) {
+                std::vector<Control*> others;
+                for (int j = 0; j < py; ++j)
+                    if (j != k) others.push_back(g->strips[j]->ctl);
+                cudaSetDevice(g->strips[k]->device);
+                if (cudaMalloc(&g->peers[k], others.size() * sizeof(Control*)) != cudaSuccess ||
+                    cudaMemcpy(g->peers[k], others.data(), others.size() * sizeof(Control*),
+                               cudaMemcpyHostToDevice) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&g->pushed[k], cudaEventDisableTiming) != cudaSuccess)
+                    ok = false;
+            }
+            g->direct = ok;
+            if (!ok) {
+                silt_group_destroy(g);
+                return fail(SILT_ERR_CUDA, "silt_group_create: direct-mode setup failed");
+            }
+        }
+    }
     cudaSetDevice(g->dev0);
     if (cudaStreamCreateWithFlags(&g->s0, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&g->reduced, cudaEventDisableTiming) != cudaSuccess ||
@@ -1135,10 +1210,31 @@ int silt_group_begin(silt_group* g, const silt_run_plan* plan) {
 
 int silt_group_step(silt_group* g, int n) {
     if (!g) return fail(SILT_ERR_INVALID, "null group");
+    const int py = (int)g->strips.size();
     for (int k = 0; k < n; ++k) {
-        for (silt_solver* s : g->strips)
+        if (!g->direct) {
+            for (silt_solver* s : g->strips)
+                if (int rc = silt_solver_step(s, 1)) return rc;
+            if (int rc = group_exchange(g)) return rc;
+            continue;
+        }
+        for (int i = 0; i < py; ++i) {
+            silt_solver* s = g->strips[i];
+            CUDA_TRY(cudaSetDevice(s->device));
+            // every strip's previous step (rows delivered, maxima pushed) is
+            // done: one join event (2 py waits per step instead of py^2)
+            if (g->joined) CUDA_TRY(cudaStreamWaitEvent(s->stream, g->reduced, 0));
             if (int rc = silt_solver_step(s, 1)) return rc;
-        if (int rc = group_exchange(g)) return rc;
+            push_max_kernel<<<1, 32, 0, s->stream>>>(s->ctl, (int)(s->launches % 3), g->peers[i],
+                                                      py - 1);
+            ++s->kernel_count;
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaEventRecord(g->pushed[i], s->stream));
+        }
+        CUDA_TRY(cudaSetDevice(g->dev0));
+        for (int j = 0; j < py; ++j) CUDA_TRY(cudaStreamWaitEvent(g->s0, g->pushed[j], 0));
+        CUDA_TRY(cudaEventRecord(g->reduced, g->s0));
+        g->joined = true;
     }
     return SILT_OK;
 }

@@ -195,9 +195,9 @@ __device__ __forceinline__ void load_cell(const StepArgs& A, int p, int col, int
     if (row < 0 || row >= A.ny) {
         const double* g;
         if (row < 0)
-            g = A.south_nbr ? A.recv_s : A.ghost_s[p];
+            g = A.south_nbr ? A.recv_s[p] : A.ghost_s[p];
         else
-            g = A.north_nbr ? A.recv_n : A.ghost_n[p];
+            g = A.north_nbr ? A.recv_n[p] : A.ghost_n[p];
         const int cc = min(max(col, 0), nx - 1);
 #pragma unroll
         for (int f = 0; f < 4; ++f) c[f] = g[(size_t)f * nx + cc];
@@ -235,7 +235,7 @@ __device__ __forceinline__ void write_edges(const StepArgs& A, int q, int col, i
     if (row == 0) {
         if (A.south_nbr) {
 #pragma unroll
-            for (int f = 0; f < 4; ++f) A.send_s[(size_t)f * A.nx + col] = c[f];
+            for (int f = 0; f < 4; ++f) A.send_s[q][(size_t)f * A.nx + col] = c[f];
         } else if (A.per_y_self) {
 #pragma unroll
             for (int f = 0; f < 4; ++f) A.ghost_n[q][(size_t)f * A.nx + col] = c[f];
@@ -249,7 +249,7 @@ __device__ __forceinline__ void write_edges(const StepArgs& A, int q, int col, i
     if (row == A.ny - 1) {
         if (A.north_nbr) {
 #pragma unroll
-            for (int f = 0; f < 4; ++f) A.send_n[(size_t)f * A.nx + col] = c[f];
+            for (int f = 0; f < 4; ++f) A.send_n[q][(size_t)f * A.nx + col] = c[f];
         } else if (A.per_y_self) {
 #pragma unroll
             for (int f = 0; f < 4; ++f) A.ghost_s[q][(size_t)f * A.nx + col] = c[f];
@@ -396,8 +396,8 @@ __device__ __forceinline__ RowSrc row_src(const StepArgs& A, int p, int col) {
 __device__ __forceinline__ const double* row_field(const StepArgs& A, const RowSrc& s, int p,
                                                    int row, int f) {
     if (row >= 0 && row < A.ny) return s.base + (size_t)f * s.fstride + (size_t)row * s.stride;
-    const double* g = row < 0 ? (A.south_nbr ? A.recv_s : A.ghost_s[p])
-                              : (A.north_nbr ? A.recv_n : A.ghost_n[p]);
+    const double* g = row < 0 ? (A.south_nbr ? A.recv_s[p] : A.ghost_s[p])
+                              : (A.north_nbr ? A.recv_n[p] : A.ghost_n[p]);
     return g + (size_t)f * A.nx + s.col_clamped;
 }
 

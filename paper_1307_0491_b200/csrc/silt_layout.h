@@ -5,7 +5,8 @@
 //                  pitch = nx rounded up to 32 doubles (256 B rows)
 //   ghost_s/n[2] : ghost rows -1 / ny per parity, [4][nx] (physical BC rows,
 //                  periodic self-wrap or caller-given rows)
-//   recv_s/n     : ghost rows received from neighbour strips, [4][nx]
+//   recv_s/n     : ghost rows received from neighbour strips, [4][nx] (x2 parities
+//                  in the group's direct mode)
 //   send_s/n     : edge rows 0 / ny-1 for neighbour strips, [4][nx]
 //   ghost_w/e    : caller-given ghost columns (SILT_BC_GIVEN), [4][ny]
 //   Control      : triple-buffered run-clock/reduction mailboxes
@@ -83,10 +84,15 @@ struct StepArgs {
     double* state[2][4];
     double* ghost_s[2];
     double* ghost_n[2];
-    double* recv_s;
-    double* recv_n;
-    double* send_s;
-    double* send_n;
+    // Ghost rows from / edge rows for neighbour strips, per state parity:
+    // step n reads recv_*[n & 1] and writes send_*[(n + 1) & 1].  A driver
+    // that copies rows between steps points both parities at one buffer; the
+    // in-process group's direct mode points send_* at the neighbours' recv_*
+    // (peer memory), so the step kernel itself delivers the rows.
+    double* recv_s[2];
+    double* recv_n[2];
+    double* send_s[2];
+    double* send_n[2];
     double* ghost_w;
     double* ghost_e;
     Control* ctl;
