@@ -254,6 +254,31 @@ int silt_solver_exchange_ptrs(silt_solver* s, silt_exchange* out);
  * enough to use the dynamic row-block order): use silt_solver_step. */
 int silt_solver_step_split_ok(silt_solver* s, int* ok);
 int silt_solver_step_part(silt_solver* s, int part);
+/* ---- multi-process strips over peer memory (CUDA IPC) ----------------------
+ * The step exchange without a collective library: every rank exports its
+ * exchange rows, Control block and step-flag array; after connect, the step
+ * kernel stores the strip's edge rows straight into the neighbours' receive
+ * rows (double-buffered by state parity), a one-warp kernel folds the strip's
+ * axis-speed maxima into every rank's slot with remote atomics, and the
+ * stream writes its step count into every rank's flag array; the next step
+ * waits (a stream memory operation, no host synchronisation) until every
+ * rank's count has arrived.  Replaces halo_exchange + global_dt
+ * (src/parallel.cpp:43-99, 192-206) of run_parallel's loop.
+ * Protocol: create all strips, begin, export, all-gather the handles
+ * (any host channel), connect, then one MAX all-reduce of the slot (e.g. the
+ * same channel) to finish begin's reduction; from then on silt_solver_p2p_step
+ * on every rank with the same n. */
+typedef struct silt_p2p_handle {
+    char rows[64];   /* cudaIpcMemHandle_t of the exchange-row buffer */
+    char ctl[64];    /* ... of the Control block */
+    char flags[64];  /* ... of the step-flag array */
+    int32_t nx;
+    int32_t pad_;
+} silt_p2p_handle;
+int silt_solver_p2p_export(silt_solver* s, silt_p2p_handle* out);
+int silt_solver_p2p_connect(silt_solver* s, int rank, int world, const silt_p2p_handle* all,
+                            int south_rank, int north_rank);
+int silt_solver_p2p_step(silt_solver* s, int n);
 /* Number of kernel launches this handle has enqueued (for accounting). */
 int silt_solver_launch_count(silt_solver* s, int64_t* count);
 

@@ -5,6 +5,7 @@
 // kernels on the solver's stream and maps device error words back onto the
 // reference's exception classes (status codes SILT_ERR_INVALID ~
 // std::invalid_argument, SILT_ERR_RUNTIME ~ std::runtime_error).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -167,6 +168,13 @@ struct silt_solver {
     int row_blocks = 0;
     int rb_span = 900;          // hot row blocks spread over this share (per mille) of a launch
     int coop_blocks = -1;       // 1D: co-resident CTAs of the cooperative step kernel (-1: unknown)
+    // multi-process peer-memory exchange (silt_solver_p2p_*)
+    unsigned* p2p_flags = nullptr;       // [64]: step count of every rank (written by the ranks)
+    int p2p_rank = -1, p2p_world = 0;
+    unsigned p2p_count = 0;              // steps taken through silt_solver_p2p_step
+    std::vector<void*> p2p_opened;       // IPC mappings to close
+    std::vector<unsigned*> p2p_peer_flag;  // per other rank: &their_flags[p2p_rank]
+    Control** p2p_peer_ctl = nullptr;    // device array: the other ranks' Control
     bool cluster_failed = false;  // 1D: the cluster launch was refused once
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
     cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
@@ -513,6 +521,9 @@ int silt_solver_destroy(silt_solver* s) {
     cudaFree(s->snapbuf);
     cudaFree(s->rb_mem);
     cudaFree(s->split_map);
+    for (void* p : s->p2p_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(s->p2p_peer_ctl);
+    cudaFree(s->p2p_flags);
     cudaFree(s->planes);
     cudaFree(s->rows);
     cudaFree(s->cols);
@@ -1776,5 +1787,137 @@ extern "C" int silt_solver_capture_write(silt_solver* s, double time, const char
         s->writer_rc = rc;
         if (rc != SILT_OK) s->writer_err = silt_last_error();
     });
+    return SILT_OK;
+}
+
+// ---- multi-process strips over peer memory ----------------------------------------
+namespace {
+
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+int stream_mem_ops(WaitValueFn* wait, WriteValueFn* write) {
+    static WaitValueFn w = nullptr;
+    static WriteValueFn r = nullptr;
+    if (!w || !r) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) !=
+                cudaSuccess || !f)
+            return fail(SILT_ERR_UNSUPPORTED, "p2p: cuStreamWaitValue32 unavailable");
+        w = reinterpret_cast<WaitValueFn>(f);
+        f = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) !=
+                cudaSuccess || !f)
+            return fail(SILT_ERR_UNSUPPORTED, "p2p: cuStreamWriteValue32 unavailable");
+        r = reinterpret_cast<WriteValueFn>(f);
+    }
+    *wait = w;
+    *write = r;
+    return SILT_OK;
+}
+
+}  // namespace
+
+extern "C" int silt_solver_p2p_export(silt_solver* s, silt_p2p_handle* out) {
+    if (!s || !out) return fail(SILT_ERR_INVALID, "silt_solver_p2p_export: null argument");
+    if (s->prob.dim != 2) return fail(SILT_ERR_UNSUPPORTED, "p2p: 2D strips only");
+    CUDA_TRY(cudaSetDevice(s->device));
+    if (!s->p2p_flags) {
+        CUDA_TRY(cudaMalloc(&s->p2p_flags, 64 * sizeof(unsigned)));
+        CUDA_TRY(cudaMemset(s->p2p_flags, 0, 64 * sizeof(unsigned)));
+    }
+    std::memset(out, 0, sizeof *out);
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, s->rows));
+    std::memcpy(out->rows, &h, sizeof h);
+    CUDA_TRY(cudaIpcGetMemHandle(&h, s->ctl));
+    std::memcpy(out->ctl, &h, sizeof h);
+    CUDA_TRY(cudaIpcGetMemHandle(&h, s->p2p_flags));
+    std::memcpy(out->flags, &h, sizeof h);
+    out->nx = s->nx;
+    return SILT_OK;
+}
+
+extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
+                                       const silt_p2p_handle* all, int south, int north) {
+    if (!s || !all) return fail(SILT_ERR_INVALID, "silt_solver_p2p_connect: null argument");
+    if (world < 2 || world > 64 || rank < 0 || rank >= world)
+        return fail(SILT_ERR_INVALID, "p2p: 2 <= world <= 64, 0 <= rank < world");
+    if (!s->p2p_flags) return fail(SILT_ERR_INVALID, "p2p: export before connect");
+    if ((south >= 0) != (bool)s->strip.south_neighbor || (north >= 0) != (bool)s->strip.north_neighbor)
+        return fail(SILT_ERR_INVALID, "p2p: neighbours do not match the strip");
+    WaitValueFn w;
+    WriteValueFn r;
+    if (int rc = stream_mem_ops(&w, &r)) return rc;
+    CUDA_TRY(cudaSetDevice(s->device));
+    std::vector<void*> rows(world, nullptr), ctls(world, nullptr), flags(world, nullptr);
+    for (int j = 0; j < world; ++j) {
+        if (j == rank) continue;
+        if (all[j].nx != s->nx) return fail(SILT_ERR_INVALID, "p2p: strips of different widths");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all[j].ctl, sizeof h);
+        CUDA_TRY(cudaIpcOpenMemHandle(&ctls[j], h, cudaIpcMemLazyEnablePeerAccess));
+        s->p2p_opened.push_back(ctls[j]);
+        std::memcpy(&h, all[j].flags, sizeof h);
+        CUDA_TRY(cudaIpcOpenMemHandle(&flags[j], h, cudaIpcMemLazyEnablePeerAccess));
+        s->p2p_opened.push_back(flags[j]);
+        if (j == south || j == north) {
+            std::memcpy(&h, all[j].rows, sizeof h);
+            CUDA_TRY(cudaIpcOpenMemHandle(&rows[j], h, cudaIpcMemLazyEnablePeerAccess));
+            s->p2p_opened.push_back(rows[j]);
+        }
+    }
+    const size_t row = 4 * (size_t)s->nx;
+    StepArgs& A = s->args;
+    A.recv_s[1] = s->rows + 8 * row;  // second parity of the receive rows
+    A.recv_n[1] = s->rows + 9 * row;
+    for (int q = 0; q < 2; ++q) {
+        if (south >= 0) A.send_s[q] = static_cast<double*>(rows[south]) + (q ? 9 : 5) * row;
+        if (north >= 0) A.send_n[q] = static_cast<double*>(rows[north]) + (q ? 8 : 4) * row;
+    }
+    std::vector<Control*> others;
+    s->p2p_peer_flag.clear();
+    for (int j = 0; j < world; ++j) {
+        if (j == rank) continue;
+        others.push_back(static_cast<Control*>(ctls[j]));
+        s->p2p_peer_flag.push_back(static_cast<unsigned*>(flags[j]) + rank);
+    }
+    CUDA_TRY(cudaMalloc(&s->p2p_peer_ctl, others.size() * sizeof(Control*)));
+    CUDA_TRY(cudaMemcpy(s->p2p_peer_ctl, others.data(), others.size() * sizeof(Control*),
+                        cudaMemcpyHostToDevice));
+    s->p2p_rank = rank;
+    s->p2p_world = world;
+    return SILT_OK;
+}
+
+extern "C" int silt_solver_p2p_step(silt_solver* s, int n) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    if (s->p2p_world < 2) return fail(SILT_ERR_INVALID, "silt_solver_p2p_step: not connected");
+    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_p2p_step: call silt_solver_begin first");
+    if (int rc = check_cfl(s->prob.cfl)) return rc;
+    WaitValueFn wait;
+    WriteValueFn write;
+    if (int rc = stream_mem_ops(&wait, &write)) return rc;
+    CUDA_TRY(cudaSetDevice(s->device));
+    const CUstream cs = reinterpret_cast<CUstream>(s->stream);
+    for (int k = 0; k < n; ++k) {
+        const unsigned c = ++s->p2p_count;
+        if (c > 1)  // every rank finished step c-1: its rows and maxima are here
+            for (int j = 0; j < s->p2p_world; ++j) {
+                if (j == s->p2p_rank) continue;
+                if (wait(cs, reinterpret_cast<CUdeviceptr>(s->p2p_flags + j), c - 1,
+                         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                    return fail(SILT_ERR_CUDA, "p2p: cuStreamWaitValue32 failed");
+            }
+        launch_step(s);
+        push_max_kernel<<<1, 32, 0, s->stream>>>(s->ctl, (int)(s->launches % 3), s->p2p_peer_ctl,
+                                                  s->p2p_world - 1);
+        ++s->kernel_count;
+        CUDA_TRY(cudaGetLastError());
+        for (unsigned* f : s->p2p_peer_flag)
+            if (write(cs, reinterpret_cast<CUdeviceptr>(f), c, 0) != CUDA_SUCCESS)
+                return fail(SILT_ERR_CUDA, "p2p: cuStreamWriteValue32 failed");
+    }
     return SILT_OK;
 }

@@ -209,13 +209,49 @@ class StripRunner:
             # memory (used by the one-GPU multi-process tests; NCCL moves the
             # device buffers directly)
             self._stage = self.torch_stream is not None and dist.get_backend() == "gloo"
+        # Peer-memory exchange (silt_solver_p2p_*): the step kernels deliver
+        # the edge rows into the neighbours' memory and the maxima by remote
+        # atomics, ordered by stream memory operations — no collective per
+        # step.  Every rank must succeed, else all use the collective path.
+        # SILT_P2P=0 disables.
+        self._p2p = False
+        if (world > 1 and self.torch_stream is not None and problem.dim == 2 and
+                os.environ.get("SILT_P2P", "1") != "0"):
+            self._p2p = self._setup_p2p()
         # halo/compute overlap (silt_solver_step_part); SILT_OVERLAP=0 disables
-        self._overlap = (world > 1 and self.torch_stream is not None and
+        self._overlap = (not self._p2p and world > 1 and self.torch_stream is not None and
                          os.environ.get("SILT_OVERLAP", "1") != "0" and self.solver.split_ok())
         if self._overlap and not self._stage:
             import torch
             self._comm = torch.cuda.Stream(device=self.device)
             self._ev = torch.cuda.Event()
+
+    def _setup_p2p(self) -> bool:
+        import torch
+        dist = self._dist
+        ok = 1
+        handle = b""
+        try:
+            handle = self.solver.p2p_export()
+        except Exception:
+            ok = 0
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle)
+        if ok and all(handles):
+            try:
+                self.solver.p2p_connect(self.rank, self.world, handles, self.south, self.north)
+            except Exception:
+                ok = 0
+        else:
+            ok = 0
+        t = torch.tensor([ok], dtype=torch.int32,
+                         device=self.device if not self._stage else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) != 1:
+            if ok:  # connected here but not everywhere: not usable
+                raise RuntimeError("p2p: connected on some ranks only")
+            return False
+        return True
 
     def _wrap(self, ptr, n):
         if not ptr:
@@ -346,12 +382,21 @@ class StripRunner:
         with self._ctx():
             self.solver.begin(t_end=t_end, max_steps=max_steps, snapshots=snapshots,
                               dt_cap=dt_cap)
-            self._exchange()
+            if self._p2p:
+                # the initial reduction delivered the edge rows itself; the
+                # MAX all-reduce finishes global_dt and orders every rank's
+                # initial kernels before any first step
+                self._reduce_slot()
+            else:
+                self._exchange()
 
     def step(self, n: int = 1):
         with self._ctx():
             if self.world == 1:
                 self.solver.step(n)
+                return
+            if self._p2p:
+                self.solver.p2p_step(n)
                 return
             for _ in range(n):
                 if self._overlap:

@@ -101,6 +101,9 @@ def lib() -> C.CDLL:
         "silt_host_alloc": ([C.c_int64, C.POINTER(_VP)], C.c_int),
         "silt_host_free": ([_VP], C.c_int),
         "silt_solver_step_split_ok": ([_VP, C.POINTER(C.c_int)], C.c_int),
+        "silt_solver_p2p_export": ([_VP, C.c_void_p], C.c_int),
+        "silt_solver_p2p_connect": ([_VP, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int], C.c_int),
+        "silt_solver_p2p_step": ([_VP, C.c_int], C.c_int),
         "silt_solver_step_part": ([_VP, C.c_int], C.c_int),
         "silt_snapshot_to_string": ([_P, _VP, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                      C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
@@ -276,6 +279,21 @@ class Solver:
 
     def step(self, n: int = 1):
         check(self.L.silt_solver_step(self.h, int(n)))
+
+    # multi-process peer-memory exchange (silt_solver_p2p_*)
+    def p2p_export(self) -> bytes:
+        buf = C.create_string_buffer(200)
+        check(self.L.silt_solver_p2p_export(self.h, buf))
+        return buf.raw[:200]
+
+    def p2p_connect(self, rank: int, world: int, handles, south, north):
+        blob = b"".join(handles)
+        check(self.L.silt_solver_p2p_connect(self.h, rank, world, blob,
+                                             -1 if south is None else south,
+                                             -1 if north is None else north))
+
+    def p2p_step(self, n: int = 1):
+        check(self.L.silt_solver_p2p_step(self.h, int(n)))
 
     def split_ok(self) -> bool:
         ok = C.c_int(0)

@@ -1,6 +1,11 @@
 """GPU, multi-process: the row-strip driver (StripRunner) with the real CUDA
 solver in every rank, on one B200.
 
+With SILT_P2P unset (default) the ranks exchange over peer memory (CUDA IPC:
+the step kernels store edge rows into the neighbours' buffers, maxima by
+remote atomics, stream memory operations order the steps); SILT_P2P=0 runs
+the collective path (here gloo, host-staged; NCCL on the multi-GPU box).
+
 The round-end and SCALE runs use StripRunner over NCCL with one GPU per rank;
 a gpurun box has one GPU and NCCL refuses two ranks on one device, so these
 ranks talk over gloo (edge rows and the speed slot staged through host
@@ -53,6 +58,7 @@ def _worker(rank, world, port, case, out_dir, variant, partition):
     if rank == 0:
         np.save(os.path.join(out_dir, "field.npy"), field)
         np.save(os.path.join(out_dir, "meta.npy"), np.array([st.t, st.steps] + seen))
+        np.save(os.path.join(out_dir, "mode.npy"), np.array([runner._p2p, runner._overlap]))
     runner.close()
     runner.shutdown()
 
@@ -72,6 +78,8 @@ def test_strip_runner_ranks_on_one_gpu(tmp_path, golden, world, case):
                  nprocs=world, join=True)
         field = np.load(out / "field.npy")
         mt = np.load(out / "meta.npy")
+        p2p, _ = np.load(out / "mode.npy")
+        assert bool(p2p) == (os.environ.get("SILT_P2P", "1") != "0")  # the path under test
         assert mt[1] == m["steps"]
         assert list(mt[2:]) == [s for s in m["snapshots"] if s <= m["t_final"]]
         if variant == abi.VARIANT_STRICT:
