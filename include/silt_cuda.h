@@ -264,10 +264,11 @@ int silt_solver_step_part(silt_solver* s, int part);
  * waits (a stream memory operation, no host synchronisation) until every
  * rank's count has arrived.  Replaces halo_exchange + global_dt
  * (src/parallel.cpp:43-99, 192-206) of run_parallel's loop.
- * Protocol: create all strips, begin, export, all-gather the handles
- * (any host channel), connect, then one MAX all-reduce of the slot (e.g. the
- * same channel) to finish begin's reduction; from then on silt_solver_p2p_step
- * on every rank with the same n. */
+ * Protocol: create the strip, export, all-gather the handles (any host
+ * channel), connect; then per run: begin (its initial reduction already
+ * stores the edge rows into the neighbours' memory), one MAX all-reduce of
+ * the slot over the same channel (finishes global_dt and orders every rank's
+ * initial kernels), and silt_solver_p2p_step on every rank with the same n. */
 typedef struct silt_p2p_handle {
     char rows[64];   /* cudaIpcMemHandle_t of the exchange-row buffer */
     char ctl[64];    /* ... of the Control block */
