@@ -172,6 +172,7 @@ struct silt_solver {
     unsigned* p2p_flags = nullptr;       // [64]: step count of every rank (written by the ranks)
     int p2p_rank = -1, p2p_world = 0;
     unsigned p2p_count = 0;              // steps taken through silt_solver_p2p_step
+    bool begun_after_connect = false;    // the run's initial rows went to the peers
     std::vector<void*> p2p_opened;       // IPC mappings to close
     std::vector<unsigned*> p2p_peer_flag;  // per other rank: &their_flags[p2p_rank]
     Control** p2p_peer_ctl = nullptr;    // device array: the other ranks' Control
@@ -773,6 +774,7 @@ int silt_solver_begin(silt_solver* s, const silt_run_plan* plan) {
     ++s->kernel_count;
     CUDA_TRY(cudaGetLastError());
     s->begun = true;
+    s->begun_after_connect = s->p2p_world > 1;
     return SILT_OK;
 }
 
@@ -1888,13 +1890,15 @@ extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
                         cudaMemcpyHostToDevice));
     s->p2p_rank = rank;
     s->p2p_world = world;
+    s->begun_after_connect = false;
     return SILT_OK;
 }
 
 extern "C" int silt_solver_p2p_step(silt_solver* s, int n) {
     if (!s) return fail(SILT_ERR_INVALID, "null solver");
     if (s->p2p_world < 2) return fail(SILT_ERR_INVALID, "silt_solver_p2p_step: not connected");
-    if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_p2p_step: call silt_solver_begin first");
+    if (!s->begun || !s->begun_after_connect)
+        return fail(SILT_ERR_INVALID, "silt_solver_p2p_step: call silt_solver_begin after connect");
     if (int rc = check_cfl(s->prob.cfl)) return rc;
     WaitValueFn wait;
     WriteValueFn write;
