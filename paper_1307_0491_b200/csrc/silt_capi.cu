@@ -1888,6 +1888,20 @@ extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
     CUDA_TRY(cudaMalloc(&s->p2p_peer_ctl, others.size() * sizeof(Control*)));
     CUDA_TRY(cudaMemcpy(s->p2p_peer_ctl, others.data(), others.size() * sizeof(Control*),
                         cudaMemcpyHostToDevice));
+    // probe the mechanism once (remote atomics, remote flag writes, local
+    // waits) so that a driver can fall back before its first step
+    {
+        const CUstream cs = reinterpret_cast<CUstream>(s->stream);
+        push_max_kernel<<<1, 32, 0, s->stream>>>(s->ctl, 0, s->p2p_peer_ctl, world - 1);
+        CUDA_TRY(cudaGetLastError());
+        for (unsigned* f : s->p2p_peer_flag)
+            if (r(cs, reinterpret_cast<CUdeviceptr>(f), s->p2p_count, 0) != CUDA_SUCCESS)
+                return fail(SILT_ERR_UNSUPPORTED, "p2p: remote stream writes unsupported");
+        if (w(cs, reinterpret_cast<CUdeviceptr>(s->p2p_flags), 0, CU_STREAM_WAIT_VALUE_GEQ) !=
+            CUDA_SUCCESS)
+            return fail(SILT_ERR_UNSUPPORTED, "p2p: stream waits unsupported");
+        CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
     s->p2p_rank = rank;
     s->p2p_world = world;
     s->begun_after_connect = false;
