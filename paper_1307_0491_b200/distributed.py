@@ -458,6 +458,11 @@ class StripRunner:
         return np.concatenate(parts, axis=0)
 
     def close(self):
+        if self._p2p:
+            # peers may still be storing into this rank's memory: every rank
+            # drains its stream before any rank frees its buffers
+            self.torch_stream.synchronize()
+            self._dist.barrier()
         self.solver.close()
 
     def shutdown(self):
