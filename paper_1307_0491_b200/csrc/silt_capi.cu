@@ -175,6 +175,7 @@ struct silt_solver {
     bool begun_after_connect = false;    // the run's initial rows went to the peers
     std::vector<void*> p2p_opened;       // IPC mappings to close
     std::vector<unsigned*> p2p_peer_flag;  // per other rank: &their_flags[p2p_rank]
+    unsigned** p2p_peer_flag_dev = nullptr;  // the same, device array
     Control** p2p_peer_ctl = nullptr;    // device array: the other ranks' Control
     bool cluster_failed = false;  // 1D: the cluster launch was refused once
     cudaStream_t copy_stream = nullptr;  // snapshot D2H, overlapping the next steps
@@ -524,6 +525,7 @@ int silt_solver_destroy(silt_solver* s) {
     cudaFree(s->split_map);
     for (void* p : s->p2p_opened) cudaIpcCloseMemHandle(p);
     cudaFree(s->p2p_peer_ctl);
+    cudaFree(s->p2p_peer_flag_dev);
     cudaFree(s->p2p_flags);
     cudaFree(s->planes);
     cudaFree(s->rows);
@@ -965,6 +967,40 @@ __global__ void push_max_kernel(const Control* local, int slot, Control* const* 
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
         atomicMax(&peers[k]->slot[slot].max_sx, sx);
         atomicMax(&peers[k]->slot[slot].max_sy, sy);
+    }
+}
+
+// p2p: maxima into the peers' slots, then (release, system scope) this rank's
+// step count into every peer's flag array: a peer that acquires the flag
+// also observes this rank's edge rows and maxima.
+__global__ void push_release_kernel(const Control* local, int slot, Control* const* peers,
+                                    unsigned* const* peer_flags, int n, unsigned value) {
+    const unsigned long long sx = local->slot[slot].max_sx, sy = local->slot[slot].max_sy;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        atomicMax(&peers[k]->slot[slot].max_sx, sx);
+        atomicMax(&peers[k]->slot[slot].max_sy, sy);
+    }
+    __syncthreads();
+    __threadfence_system();
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_flags[k]), "r"(value)
+                     : "memory");
+}
+
+// p2p: acquire (system scope) every peer's flag before the step that reads
+// their rows and maxima; the stream has already waited for the values, so
+// the loop normally exits at once
+__global__ void acquire_flags_kernel(const unsigned* flags, int world, int rank,
+                                     unsigned expect) {
+    for (int j = threadIdx.x; j < world; j += blockDim.x) {
+        if (j == rank) continue;
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + j)
+                         : "memory");
+            if ((int)(v - expect) >= 0) break;
+            __nanosleep(1000);
+        }
     }
 }
 
@@ -1888,18 +1924,23 @@ extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
     CUDA_TRY(cudaMalloc(&s->p2p_peer_ctl, others.size() * sizeof(Control*)));
     CUDA_TRY(cudaMemcpy(s->p2p_peer_ctl, others.data(), others.size() * sizeof(Control*),
                         cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&s->p2p_peer_flag_dev, s->p2p_peer_flag.size() * sizeof(unsigned*)));
+    CUDA_TRY(cudaMemcpy(s->p2p_peer_flag_dev, s->p2p_peer_flag.data(),
+                        s->p2p_peer_flag.size() * sizeof(unsigned*), cudaMemcpyHostToDevice));
     // probe the mechanism once (remote atomics, remote flag writes, local
     // waits) so that a driver can fall back before its first step
     {
         const CUstream cs = reinterpret_cast<CUstream>(s->stream);
-        push_max_kernel<<<1, 32, 0, s->stream>>>(s->ctl, 0, s->p2p_peer_ctl, world - 1);
+        push_release_kernel<<<1, 32, 0, s->stream>>>(s->ctl, 0, s->p2p_peer_ctl,
+                                                     s->p2p_peer_flag_dev, world - 1,
+                                                     s->p2p_count);
         CUDA_TRY(cudaGetLastError());
-        for (unsigned* f : s->p2p_peer_flag)
-            if (r(cs, reinterpret_cast<CUdeviceptr>(f), s->p2p_count, 0) != CUDA_SUCCESS)
-                return fail(SILT_ERR_UNSUPPORTED, "p2p: remote stream writes unsupported");
+        (void)r;
         if (w(cs, reinterpret_cast<CUdeviceptr>(s->p2p_flags), 0, CU_STREAM_WAIT_VALUE_GEQ) !=
             CUDA_SUCCESS)
             return fail(SILT_ERR_UNSUPPORTED, "p2p: stream waits unsupported");
+        acquire_flags_kernel<<<1, 32, 0, s->stream>>>(s->p2p_flags, world, rank, 0u);
+        CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(s->stream));
     }
     s->p2p_rank = rank;
@@ -1919,23 +1960,29 @@ extern "C" int silt_solver_p2p_step(silt_solver* s, int n) {
     if (int rc = stream_mem_ops(&wait, &write)) return rc;
     CUDA_TRY(cudaSetDevice(s->device));
     const CUstream cs = reinterpret_cast<CUstream>(s->stream);
+    (void)write;
     for (int k = 0; k < n; ++k) {
         const unsigned c = ++s->p2p_count;
-        if (c > 1)  // every rank finished step c-1: its rows and maxima are here
+        if (c > 1) {
+            // every rank finished step c-1 (its rows and maxima are here): the
+            // stream waits without occupying the GPU, then one thread acquires
+            // the flags at system scope so the step observes the peers' writes
             for (int j = 0; j < s->p2p_world; ++j) {
                 if (j == s->p2p_rank) continue;
                 if (wait(cs, reinterpret_cast<CUdeviceptr>(s->p2p_flags + j), c - 1,
                          CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                     return fail(SILT_ERR_CUDA, "p2p: cuStreamWaitValue32 failed");
             }
+            acquire_flags_kernel<<<1, 32, 0, s->stream>>>(s->p2p_flags, s->p2p_world, s->p2p_rank,
+                                                          c - 1);
+            ++s->kernel_count;
+        }
         launch_step(s);
-        push_max_kernel<<<1, 32, 0, s->stream>>>(s->ctl, (int)(s->launches % 3), s->p2p_peer_ctl,
-                                                  s->p2p_world - 1);
+        push_release_kernel<<<1, 32, 0, s->stream>>>(s->ctl, (int)(s->launches % 3),
+                                                     s->p2p_peer_ctl, s->p2p_peer_flag_dev,
+                                                     s->p2p_world - 1, c);
         ++s->kernel_count;
         CUDA_TRY(cudaGetLastError());
-        for (unsigned* f : s->p2p_peer_flag)
-            if (write(cs, reinterpret_cast<CUdeviceptr>(f), c, 0) != CUDA_SUCCESS)
-                return fail(SILT_ERR_CUDA, "p2p: cuStreamWriteValue32 failed");
     }
     return SILT_OK;
 }
