@@ -514,11 +514,11 @@ __device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], S
 // SILT_RING: cp.async ring slots; rows are issued SILT_RING-1 ahead
 // Per-CTA shared memory of the 2D step (dynamic: above the 48 KB static cap).
 struct StepSmem {
+    double row[SILT_RING][4][kStepThreads];  // cp.async ring
     double side[11][kStepThreads];        // y-side terms of row r-1
     double sx[11][kStepThreads + 1];      // x-side terms of row r (+1: lane 31 reads t+1)
     double xs[4][kStepThreads];           // x-updated row r-1
     double fy[4][kStepThreads];           // y face below row r-1: h, huR, hv, z
-    double row[SILT_RING][4][kStepThreads];  // cp.async ring
     long long cprev[4][kStepThreads];     // previous row (bits), quiescence test
     int nfull[kStepThreads / 32];         // full-path rows of each warp (launch order)
 };
