@@ -751,6 +751,9 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
 
     int it = 0;
     while (!early && res_norm(e) > tol) {
+#ifdef SILT_NEWTON_CAP  // timing experiments only: accept the iterate after CAP iterations
+        if (it >= SILT_NEWTON_CAP) break;
+#endif
         if (++it > (kTry ? kTryNewton : kMaxNewton)) return kTry ? kBail : kIllPosed;
         double j11, j12, j21, j22, det, step2, step4;
         if constexpr (S) {
