@@ -376,7 +376,6 @@ __device__ __forceinline__ RowSrc row_src(const StepArgs& A, int p, int col) {
         const int t = A.bc_type[side];
         if (t == SILT_BC_GIVEN) {
             const double* g = side == SILT_WEST ? A.ghost_w : A.ghost_e;
-#pragma unroll
             s.base = g;
             s.fstride = A.ny;
             s.stride = 1;
