@@ -15,3 +15,9 @@ extern "C" int silt_debug_stats(unsigned long long* out, int n) {
     return 0;
 }
 #endif
+
+#ifdef SILT_TRACE
+extern "C" int silt_debug_trace(unsigned long long* dev_buf) {
+    return (int)cudaMemcpyToSymbol(silt_dev::g_trace, &dev_buf, sizeof dev_buf);
+}
+#endif

@@ -450,11 +450,11 @@ __device__ __forceinline__ void cp_async_wait2() {
 #define SILT_RING 6
 #endif
 __device__ __forceinline__ void cp_async_wait_ring() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(SILT_RING - 1) : "memory");
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SILT_RING - 2) : "memory");
 }
 
 template <int W>
-__device__ __forceinline__ void side_to_ring(double (*ring)[W], const Side& s, int lane) {
+__device__ __forceinline__ void side_to_ring(double (*ring)[W], int* flags, const Side& s, int lane) {
     ring[0][lane] = s.h;
     ring[1][lane] = s.hun;
     ring[2][lane] = s.pi;
@@ -465,11 +465,11 @@ __device__ __forceinline__ void side_to_ring(double (*ring)[W], const Side& s, i
     ring[7][lane] = s.tau;
     ring[8][lane] = s.a_side;
     ring[9][lane] = s.b2_side;
-    ring[10][lane] = __hiloint2double(0, s.wet | (s.moving << 1));
+    flags[lane] = s.wet | (s.moving << 1);
 }
 
 template <int W>
-__device__ __forceinline__ Side side_from_ring(const double (*ring)[W], int lane) {
+__device__ __forceinline__ Side side_from_ring(const double (*ring)[W], const int* flags, int lane) {
     Side s;
     s.h = ring[0][lane];
     s.hun = ring[1][lane];
@@ -481,7 +481,7 @@ __device__ __forceinline__ Side side_from_ring(const double (*ring)[W], int lane
     s.tau = ring[7][lane];
     s.a_side = ring[8][lane];
     s.b2_side = ring[9][lane];
-    const int fl = __double2loint(ring[10][lane]);
+    const int fl = flags[lane];
     s.wet = fl & 1;
     s.moving = (fl >> 1) & 1;
     return s;
@@ -514,11 +514,12 @@ __device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], S
 // Per-CTA shared memory of the 2D step (dynamic: above the 48 KB static cap).
 struct StepSmem {
     double row[SILT_RING][4][kStepThreads];  // cp.async ring
-    double side[11][kStepThreads];        // y-side terms of row r-1
-    double sx[11][kStepThreads + 1];      // x-side terms of row r (+1: lane 31 reads t+1)
+    double side[10][kStepThreads];        // y-side terms of row r-1
+    double sx[10][kStepThreads + 1];      // x-side terms of row r (+1: lane 31 reads t+1)
+    int side_fl[kStepThreads];            // their wet / moving flags
+    int sx_fl[kStepThreads + 1];
     double xs[4][kStepThreads];           // x-updated row r-1
     double fy[4][kStepThreads];           // y face below row r-1: h, huR, hv, z
-    long long cprev[4][kStepThreads];     // previous row (bits), quiescence test
     int nfull[kStepThreads / 32];         // full-path rows of each warp (launch order)
 };
 
@@ -537,7 +538,6 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     auto& sh_xs = sm.xs;
     auto& sh_fy = sm.fy;
     auto& sh_row = sm.row;
-    auto& sh_cprev = sm.cprev;
 
     const Slot cur = A.ctl->slot[li % 3];
     const RunDecision d = decide(A, cur);
@@ -559,6 +559,10 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const int je = min(jb + A.rows_per_block, A.ny);
     if (jb >= je) return;
     if (lane == 0) sm.nfull[t >> 5] = 0;
+#ifdef SILT_TRACE
+    unsigned long long tr_start = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
+#endif
     const double cx = d.dt / A.dx;
     const double cy = d.dt / A.dy;
     const double href = __longlong_as_double((long long)cur.hmax);
@@ -587,14 +591,25 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     double qsx = 0.0, qsy = 0.0;
 #pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
-        const int ahead = buf == 0 ? SILT_RING - 1 : buf - 1;  // slot of row r+RING-1
-        if (r + SILT_RING - 1 <= je)
-            prefetch_row(A, src, p, r + SILT_RING - 1, row_sa0 + ahead * kSlotBytes);
-        cp_async_commit();
+        // The slot of row r-1 is refilled (with row r+RING-1) only after row r
+        // has been compared with it: RING-1 rows stay in flight while row r is
+        // processed, and the quiescence test needs no copy of the previous row.
+        const int prev = buf == 0 ? SILT_RING - 1 : buf - 1;  // slot of row r-1
         cp_async_wait_ring();  // row r landed; the later rows may be in flight
         double c[4];
+        unsigned long long dif = 0;  // row r vs row r-1, bitwise (as loaded)
 #pragma unroll
-        for (int f = 0; f < 4; ++f) c[f] = sh_row[buf][f][t];
+        for (int f = 0; f < 4; ++f) {
+            c[f] = sh_row[buf][f][t];
+            if constexpr (!S)
+                dif |= (unsigned long long)(__double_as_longlong(c[f]) ^
+                                            __double_as_longlong(sh_row[prev][f][t]));
+        }
+        // every lane's reads of slot `prev` precede the refill (lanes of a
+        // warp only ever touch their own column of a slot)
+        if (r + SILT_RING - 1 <= je)
+            prefetch_row(A, src, p, r + SILT_RING - 1, row_sa0 + prev * kSlotBytes);
+        cp_async_commit();
         buf = buf == SILT_RING - 1 ? 0 : buf + 1;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
@@ -604,13 +619,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                 // vertical equality first (cheap); the horizontal test with
                 // shuffles only when the whole warp passed it
                 long long cb[4];
-                unsigned long long dif = 0;
 #pragma unroll
-                for (int f = 0; f < 4; ++f) {
-                    cb[f] = __double_as_longlong(c[f]);
-                    dif |= (unsigned long long)(cb[f] ^ sh_cprev[f][t]);
-                    sh_cprev[f][t] = cb[f];
-                }
+                for (int f = 0; f < 4; ++f) cb[f] = __double_as_longlong(c[f]);
                 const bool eqy = r > jb - 1 && dif == 0ull;
                 // Inside a streak one vote suffices: if every lane (halo and
                 // dead lanes included) sees row r equal to row r-1, and row r-1
@@ -657,15 +667,15 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         {
             Side sx, sy;
             sides_of<S, SH>(A, c, sx, sy);
-            if (own_row) side_to_ring(sh_sx, sx, t);
+            if (own_row) side_to_ring(sh_sx, sm.sx_fl, sx, t);
             if (r > jb - 1 && owned) {
-                const Side lo = side_from_ring(sh_side, t);
+                const Side lo = side_from_ring(sh_side, sm.side_fl, t);
                 if (!face_flux<S>(A.P, lo, sy, fy)) {
                     const double info[6] = {lo.h, lo.un, lo.z, sy.h, sy.un, sy.z};
                     record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
                 }
             }
-            side_to_ring(sh_side, sy, t);
+            side_to_ring(sh_side, sm.side_fl, sy, t);
         }
         if (r - 1 >= jb && owned) {
             // y update of row r-1 (src/stepper.cpp:181-186) + check_depth
@@ -694,8 +704,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         // x faces: this lane solves the face between col and col+1
         Flux fx{0, 0, 0, 0, 0};
         if (xface) {
-            const Side sx = side_from_ring(sh_sx, t);
-            const Side right = side_from_ring(sh_sx, t + 1);
+            const Side sx = side_from_ring(sh_sx, sm.sx_fl, t);
+            const Side right = side_from_ring(sh_sx, sm.sx_fl, t + 1);
             if (!face_flux<S>(A.P, sx, right, fx)) {
                 const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
                 record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
@@ -713,6 +723,22 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     if (A.rb_order && lane == 0 && sm.nfull[t >> 5] > kHotRows)
         A.rb_hot[li][__ldg(A.rb_map + blockIdx.y)] = 1;
     reduce_flush(R, nxt);
+#ifdef SILT_TRACE
+    // (trace build only) per-warp fold into the CTA's record; the buffer is
+    // initialised to {~0, 0, 0, 0} by the tool
+    if (!S && g_trace && lane == 0) {
+        unsigned long long tr_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* rec = g_trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x);
+        atomicMin(rec, tr_start);
+        atomicMax(rec + 1, tr_end);
+        rec[2] = smid | ((unsigned long long)blockIdx.x << 16);
+        atomicAdd(rec + 3, (unsigned long long)(jb / A.rows_per_block) * (t == 0) +
+                                ((unsigned long long)sm.nfull[t >> 5] << 32));
+    }
+#endif
 }
 
 // ---- K2: 1D step (step_1d, src/stepper.cpp:118-140) ----------------------
@@ -895,6 +921,11 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
                 cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH>,                             \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,                \
                                      (int)sizeof(silt_dev::StepSmem));                           \
+                /* SILT_CARVEOUT=%: shared-memory carveout preference (A/B) */                  \
+                if (const char* cv = std::getenv("SILT_CARVEOUT"))                               \
+                    cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH>,                         \
+                                         cudaFuncAttributePreferredSharedMemoryCarveout,         \
+                                         std::atoi(cv));                                         \
                 attr_set |= 1ull << (dev_ & 63);                                                 \
             }                                                                                    \
             silt_dev::step2d_kernel<S, SH>                                                       \

@@ -22,6 +22,11 @@ namespace silt_dev {
 #ifdef SILT_STATS
 __device__ unsigned long long g_stats[8];
 #endif
+#ifdef SILT_TRACE
+// diagnostics build only: per-CTA records of the FAST 2D step kernel
+// {start ns, end ns, smid | blockIdx.x << 16, row block | full rows << 16}
+__device__ unsigned long long* g_trace;
+#endif
 
 // ---- constants (src/bedload.cpp:11, src/riemann.cpp:42-45) --------------
 constexpr double kUEps = 1e-10;
