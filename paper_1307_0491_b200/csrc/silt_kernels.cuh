@@ -589,27 +589,38 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     // skipped row of a streak), folded into the reduction once per streak.
     bool quiet_prev = false, qvalid = false;
     double qsx = 0.0, qsy = 0.0;
+    // streak loop (below): not in the warps holding an x-ghost column, whose
+    // ghost cells are transformed after the load
+    const bool xedge = i0 == 0 || i0 + kCellsPerWarp >= A.nx;
+    bool have = false, eq_have = false;  // row r already loaded by the streak loop
 #pragma unroll 1
     for (int r = jb - 1; r <= je; ++r) {
         // The slot of row r-1 is refilled (with row r+RING-1) only after row r
         // has been compared with it: RING-1 rows stay in flight while row r is
         // processed, and the quiescence test needs no copy of the previous row.
         const int prev = buf == 0 ? SILT_RING - 1 : buf - 1;  // slot of row r-1
-        cp_async_wait_ring();  // row r landed; the later rows may be in flight
         double c[4];
         unsigned long long dif = 0;  // row r vs row r-1, bitwise (as loaded)
+        if (!have) {
+            cp_async_wait_ring();  // row r landed; the later rows may be in flight
 #pragma unroll
-        for (int f = 0; f < 4; ++f) {
-            c[f] = sh_row[buf][f][t];
-            if constexpr (!S)
-                dif |= (unsigned long long)(__double_as_longlong(c[f]) ^
-                                            __double_as_longlong(sh_row[prev][f][t]));
+            for (int f = 0; f < 4; ++f) {
+                c[f] = sh_row[buf][f][t];
+                if constexpr (!S)
+                    dif |= (unsigned long long)(__double_as_longlong(c[f]) ^
+                                                __double_as_longlong(sh_row[prev][f][t]));
+            }
+            // every lane's reads of slot `prev` precede the refill (lanes of a
+            // warp only ever touch their own column of a slot)
+            if (r + SILT_RING - 1 <= je)
+                prefetch_row(A, src, p, r + SILT_RING - 1, row_sa0 + prev * kSlotBytes);
+            cp_async_commit();
+        } else {  // waited for, compared and refilled by the streak loop
+#pragma unroll
+            for (int f = 0; f < 4; ++f) c[f] = sh_row[buf][f][t];
+            dif = eq_have ? 0ull : 1ull;
+            have = false;
         }
-        // every lane's reads of slot `prev` precede the refill (lanes of a
-        // warp only ever touch their own column of a slot)
-        if (r + SILT_RING - 1 <= je)
-            prefetch_row(A, src, p, r + SILT_RING - 1, row_sa0 + prev * kSlotBytes);
-        cp_async_commit();
         buf = buf == SILT_RING - 1 ? 0 : buf + 1;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
@@ -653,6 +664,43 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                             cell_speeds<S, SH>(A, c, qsx, qsy);
                             reduce_fold(A, R, c, qsx, qsy);
                             qvalid = true;
+                        }
+                    }
+                    // Streak loop: rows r-1 and r are quiet, so row r+1 is
+                    // quiet iff every lane sees it equal to row r (the vote
+                    // above), and then row r is stored unchanged.  A short
+                    // dependency chain per row (no x-ghost fix, no second
+                    // test, the previous row from registers); the first
+                    // non-quiet row goes back to the loop above, already
+                    // loaded.  Same decisions and stores as that loop.
+                    if (!xedge) {
+#pragma unroll 1
+                        while (r < je) {
+                            const int pv = buf == 0 ? SILT_RING - 1 : buf - 1;  // slot of row r
+                            cp_async_wait_ring();  // row r+1 landed
+                            unsigned long long dn = 0;
+#pragma unroll
+                            for (int f = 0; f < 4; ++f)
+                                dn |= (unsigned long long)(__double_as_longlong(sh_row[buf][f][t]) ^
+                                                           __double_as_longlong(c[f]));
+                            if (r + SILT_RING <= je)
+                                prefetch_row(A, src, p, r + SILT_RING, row_sa0 + pv * kSlotBytes);
+                            cp_async_commit();
+                            if (!__all_sync(0xffffffffu, dn == 0ull)) {
+                                have = true;  // row r+1 is the next trip's row r
+                                eq_have = dn == 0ull;
+                                break;
+                            }
+                            buf = buf == SILT_RING - 1 ? 0 : buf + 1;
+                            if (owned) {  // row r is unchanged: o == c
+                                const size_t off = (size_t)r * A.pitch;
+                                out0[off] = c[0];
+                                out0[off + plane] = c[1];
+                                out0[off + 2 * plane] = c[2];
+                                out0[off + 3 * plane] = c[3];
+                                if (r == 0 || r == A.ny - 1) write_edges(A, q, col, r, c);
+                            }
+                            ++r;
                         }
                     }
                     continue;  // warp-uniform
