@@ -236,11 +236,18 @@ def run_reference_arm(args):
             total_secs += 1.0 / rate
             total_cells += 1.0
     value = total_cells / total_secs
+    p = build_global_problem(args.workload, args.gpus, args.law)
     line = {
         "metric": "cell-updates/s (fp64, 2D)", "value": value, "unit": "cell-updates/s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "law": args.law, "sample": desc},
+        "higher_is_better": True,
+        "scaling": "weak" if WORKLOADS[args.workload]["kind"] == "random" else "strong",
+        "dtype": "f64", "data": "synthetic",
+        # the same workload string as our arm's line; the reference runs a bounded sample of it
+        "config": {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
+                   "law": args.law, "nx": p.nx, "ny": p.ny,
+                   "parallelism": f"reference run_parallel(sc, 1, {used}) on host threads",
+                   "sample": desc},
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": used, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
