@@ -863,11 +863,23 @@ __global__ void __launch_bounds__(kStepThreads) step1d_coop_kernel(StepArgs A, i
     }
 }
 
-// The same loop for grids that fit one thread-block cluster (up to 16 CTAs of
-// 384 threads: 5760 cells, C1 and C2): the per-step barrier is the cluster's
-// hardware barrier (release / acquire at cluster scope orders the state and
-// slot writes) instead of the grid-wide software barrier.
+// Grids that fit one thread-block cluster (up to 16 CTAs of 384 threads:
+// 5760 cells, C1 and C2) keep the whole line on chip for the n steps: every
+// CTA holds its 360 cells in shared memory (double-buffered by state parity),
+// reads the two cells beyond its ends from the neighbouring CTAs' shared
+// memory (DSMEM, map_shared_rank), and reduces the axis-speed maxima / hmax /
+// wet / error bits through shared memory: a CTA partial, then one cluster
+// barrier (release / acquire at cluster scope), then every warp folds the
+// CTAs' partials.  Every thread runs the run clock itself (decide(), the same
+// arithmetic on the same inputs in every CTA), so a step needs no global
+// memory round trip; the state goes back to HBM at the end, the dt log as it
+// is made, and the final run header lands in slot (li0 + n) % 3 exactly as n
+// launches of step1d_kernel would leave it (after a stop, those launches only
+// carry the header forward).  Per-face arithmetic is step1d_body's.
 constexpr int kCluster1dThreads = 384;
+
+// Global-memory variant (step1d_body per step, the cluster barrier between
+// steps): measured faster than the resident one above 8 CTAs.
 template <bool S, bool SH>
 __global__ void __launch_bounds__(kCluster1dThreads, 1)
     step1d_cluster_kernel(StepArgs A, int li0, int n) {
@@ -876,6 +888,205 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
         step1d_body<S, SH>(A, (li0 + k) % 3);
         cl.sync();
     }
+}
+
+constexpr int kCluster1dWarps = kCluster1dThreads / 32;
+#ifndef SILT_RESIDENT_MAX_CTAS
+#define SILT_RESIDENT_MAX_CTAS 8
+#endif
+constexpr int kResidentMaxCtas = SILT_RESIDENT_MAX_CTAS;  // resident 1D kernel up to this many CTAs
+constexpr int kCluster1dCells = kCluster1dWarps * kCellsPerWarp;  // 360 per CTA
+
+template <bool S, bool SH>
+__global__ void __launch_bounds__(kCluster1dThreads, 1)
+    step1d_resident_kernel(StepArgs A, int li0, int n) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ double s_line[2][4][kCluster1dCells];  // this CTA's cells, by state parity
+    __shared__ double s_wpart[kCluster1dWarps][4];    // warp partials: sx, sy, hmax, wet|err
+    __shared__ double s_cta[2][4];                    // CTA partial, by parity of the new state
+    const Control& C = *A.ctl;
+    const int rank = (int)cl.block_rank();
+    const int nctas = (int)cl.num_blocks();
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int base = rank * kCluster1dCells;
+    const int i0 = base + w * kCellsPerWarp;
+    const int col = i0 - 1 + lane;
+    const int nx = A.nx;
+    const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < nx;
+    const bool xface = lane <= kCellsPerWarp && col <= nx - 1;
+    Slot cur = C.slot[li0 % 3];
+    // this lane's cell: interior owner CTA and index, or an x-ghost
+    int src = col;
+    if (col < -1 || col > nx) src = col < 0 ? 0 : nx - 1;  // dead lane: any valid cell
+    const int side = col < 0 ? SILT_WEST : SILT_EAST;
+    const bool ghost = col == -1 || col == nx;
+    const int bct = ghost ? A.bc_type[side] : SILT_BC_OUTFLOW;
+    if (ghost) src = (bct == SILT_BC_PERIODIC) ? (col < 0 ? nx - 1 : 0) : (col < 0 ? 0 : nx - 1);
+    const int owner = src / kCluster1dCells, idx = src - owner * kCluster1dCells;
+    double* const own_cell[2] = {&s_line[0][0][col - base], &s_line[1][0][col - base]};
+    double* const src_cell[2] = {cl.map_shared_rank(&s_line[0][0][idx], owner),
+                                 cl.map_shared_rank(&s_line[1][0][idx], owner)};
+    constexpr int kF = kCluster1dCells;  // field stride in s_line
+    {
+        const int p = (int)(cur.steps & 1);
+        if (owned)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) own_cell[p][f * kF] = A.state[p][f][col];
+    }
+    cl.sync();  // lines filled; every CTA has read the initial header
+    unsigned errb = 0;
+    for (int k = 0; k < n; ++k) {
+        const RunDecision d = decide(A, cur);
+        if (!d.run) {  // what the remaining per-step launches would carry forward
+            cur.err |= (d.next_state == SILT_STATE_FAILED && !cur.err) ? kErrDry : 0u;
+            cur.state = d.next_state;
+            break;
+        }
+        if (rank == 0 && t == 0 && C.fixed_dt <= 0 && C.dt_log && cur.steps < C.dt_cap)
+            C.dt_log[cur.steps] = d.dt;
+        const int p = (int)(cur.steps & 1), q = p ^ 1;
+        double c[4];
+        if (ghost && bct == SILT_BC_GIVEN) {
+            const double* g = side == SILT_WEST ? A.ghost_w : A.ghost_e;
+#pragma unroll
+            for (int f = 0; f < 4; ++f) c[f] = g[(size_t)f * A.ny];
+        } else {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) c[f] = src_cell[p][f * kF];
+            if (ghost && bct != SILT_BC_PERIODIC) ghost_transform(A, side, c);
+        }
+        const double c1 = d.dt / A.dx;
+        const double href = __longlong_as_double((long long)cur.hmax);
+        Side sx;
+        if constexpr (S) {
+            sx = make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3]);
+        } else {
+            const CellPre pre = cell_pre_fast<SH>(A.P, c[0], c[1], c[2], c[3]);
+            sx = make_side_fast<SH>(A.P, pre, true);
+        }
+        const Side right = shfl_down_side(sx);
+        Flux fx{0, 0, 0, 0, 0};
+        if (xface && !face_flux<S>(A.P, sx, right, fx)) {
+            errb |= kErrRiemann;
+            if (atomicCAS(&A.ctl->err_claim, 0u, 1u) == 0u) {
+                A.ctl->err_bits = kErrRiemann;
+                A.ctl->err_col = col;
+                A.ctl->err_row = 0;
+                const double info[6] = {sx.h, sx.un, sx.z, right.h, right.un, right.z};
+                for (int m = 0; m < 6; ++m) A.ctl->err_info[m] = info[m];
+            }
+        }
+        const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
+        const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
+        Reduce R{0.0, 0.0, 0.0, 0u};
+        if (owned) {
+            double o[4];
+            o[0] = c[0] - c1 * (fx.h - lh);
+            o[1] = c[1] - c1 * (fx.huL - lhuR);
+            o[2] = c[2] - c1 * (fx.hv - lhv);
+            o[3] = c[3] - c1 * (fx.z - lz);
+            if (!check_depth(o[0], href)) {
+                errb |= kErrNegDepth;
+                if (atomicCAS(&A.ctl->err_claim, 0u, 1u) == 0u) {
+                    A.ctl->err_bits = kErrNegDepth;
+                    A.ctl->err_col = col;
+                    A.ctl->err_row = 0;
+                    for (int m = 0; m < 6; ++m) A.ctl->err_info[m] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < 4; ++f) own_cell[q][f * kF] = o[f];
+            double ssx, ssy;
+            cell_speeds<S, SH>(A, o, ssx, ssy);
+            reduce_fold(A, R, o, ssx, ssy);
+        }
+        // CTA partial (max of non-negative doubles; wet and error bits OR-ed)
+        double fl = __longlong_as_double((long long)(R.wet | (errb << 1)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            R.sx = smax(R.sx, __shfl_xor_sync(0xffffffffu, R.sx, o));
+            R.sy = smax(R.sy, __shfl_xor_sync(0xffffffffu, R.sy, o));
+            R.hmax = smax(R.hmax, __shfl_xor_sync(0xffffffffu, R.hmax, o));
+            fl = __longlong_as_double(__double_as_longlong(fl) |
+                                      __double_as_longlong(__shfl_xor_sync(0xffffffffu, fl, o)));
+        }
+        if (lane == 0) {
+            s_wpart[w][0] = R.sx;
+            s_wpart[w][1] = R.sy;
+            s_wpart[w][2] = R.hmax;
+            s_wpart[w][3] = fl;
+        }
+        __syncthreads();
+        if (w == 0) {
+            double a = 0.0, b = 0.0, h = 0.0;
+            long long bits = 0;
+            if (lane < kCluster1dWarps) {
+                a = s_wpart[lane][0];
+                b = s_wpart[lane][1];
+                h = s_wpart[lane][2];
+                bits = __double_as_longlong(s_wpart[lane][3]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a = smax(a, __shfl_xor_sync(0xffffffffu, a, o));
+                b = smax(b, __shfl_xor_sync(0xffffffffu, b, o));
+                h = smax(h, __shfl_xor_sync(0xffffffffu, h, o));
+                bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+            }
+            if (lane == 0) {
+                s_cta[q][0] = a;
+                s_cta[q][1] = b;
+                s_cta[q][2] = h;
+                s_cta[q][3] = __longlong_as_double(bits);
+            }
+        }
+        cl.sync();  // the new line and the CTA partials are visible cluster-wide
+        double a = 0.0, b = 0.0, h = 0.0;
+        long long bits = 0;
+        if (lane < nctas) {
+            const double* rp = cl.map_shared_rank(&s_cta[q][0], lane);
+            a = rp[0];
+            b = rp[1];
+            h = rp[2];
+            bits = __double_as_longlong(rp[3]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = smax(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = smax(b, __shfl_xor_sync(0xffffffffu, b, o));
+            h = smax(h, __shfl_xor_sync(0xffffffffu, h, o));
+            bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+        }
+        // the header of state n+1 (control_epilogue + reduce_flush of a launch)
+        cur.t = d.t_new;
+        cur.steps = cur.steps + 1;
+        cur.last_dt = d.dt;
+        cur.snap_idx = d.snap_idx;
+        cur.state = d.next_state;
+        cur.max_sx = a > 0 ? (unsigned long long)__double_as_longlong(a) : 0ull;
+        cur.max_sy = b > 0 ? (unsigned long long)__double_as_longlong(b) : 0ull;
+        cur.hmax = h > 0 ? (unsigned long long)__double_as_longlong(h) : 0ull;
+        cur.wet = (unsigned)(bits & 1);
+        cur.err = (unsigned)(bits >> 1);
+    }
+    // state back to HBM (parity of its step count), header into the slot the
+    // next launch reads, the one after it cleared for its reductions
+    {
+        const int p = (int)(cur.steps & 1);
+        if (owned)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) A.state[p][f][col] = own_cell[p][f * kF];
+    }
+    if (rank == 0 && t == 0) {
+        Slot& fin = A.ctl->slot[(li0 + n) % 3];
+        fin = cur;
+        Slot& clr = A.ctl->slot[(li0 + n + 1) % 3];
+        clr.max_sx = clr.max_sy = clr.hmax = 0ull;
+        clr.wet = 0u;
+        clr.err = 0u;
+    }
+    cl.sync();  // no CTA leaves while its shared memory may still be read
 }
 
 // ---- initial reduction of a state (first cfl_dt + hmax + ghost rows) --------
@@ -997,8 +1208,16 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
     int NAME##_step1d_cluster(const StepArgs& A, int li0, int n, int ctas, cudaStream_t st) {    \
         StepArgs a = A;                                                                          \
         void* args[] = {&a, &li0, &n};                                                           \
-        const void* f = A.P.shields ? (const void*)silt_dev::step1d_cluster_kernel<S, true>      \
-                                    : (const void*)silt_dev::step1d_cluster_kernel<S, false>;    \
+        static const int resident_env = [] {                                                     \
+            const char* e = std::getenv("SILT_1D_RESIDENT");                                     \
+            return e ? std::atoi(e) : -1;                                                        \
+        }();                                                                                     \
+        const bool resident = resident_env >= 0 ? resident_env != 0 : ctas <= silt_dev::kResidentMaxCtas; \
+        const void* f =                                                                          \
+            resident ? (A.P.shields ? (const void*)silt_dev::step1d_resident_kernel<S, true>     \
+                                    : (const void*)silt_dev::step1d_resident_kernel<S, false>)   \
+                     : (A.P.shields ? (const void*)silt_dev::step1d_cluster_kernel<S, true>      \
+                                    : (const void*)silt_dev::step1d_cluster_kernel<S, false>);   \
         cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);              \
         cudaLaunchConfig_t cfg{};                                                                \
         cfg.gridDim = dim3(ctas);                                                                \
