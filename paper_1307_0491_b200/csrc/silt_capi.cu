@@ -482,6 +482,14 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
                 return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: device allocation failed"));
             cudaMemcpy(s->split_map, m.data(), m.size() * sizeof(int), cudaMemcpyHostToDevice);
         }
+        // A hot row block must still finish inside the launch: the shorter the
+        // launch (in waves of 3 CTAs per SM), the earlier the last one starts.
+        // 1 - 6.5 / waves: C4 on one GPU (53 waves) 0.88, its 2-strip halves
+        // (26 waves) 0.75 — measured best 0.85-0.90 and 0.60-0.75.
+        {
+            const double waves = (double)ctas / (3.0 * sms);
+            s->rb_span = (int)std::max(500.0, std::min(900.0, 1000.0 * (1.0 - 6.5 / waves)));
+        }
         if (const char* es = std::getenv("SILT_RB_SPAN")) s->rb_span = std::max(100, std::min(1000, std::atoi(es)));
         s->row_blocks = (int)nb;
         if (order) {

@@ -936,15 +936,28 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
     }
     cl.sync();  // lines filled; every CTA has read the initial header
     unsigned errb = 0;
-    for (int k = 0; k < n; ++k) {
-        const RunDecision d = decide(A, cur);
-        if (!d.run) {  // what the remaining per-step launches would carry forward
-            cur.err |= (d.next_state == SILT_STATE_FAILED && !cur.err) ? kErrDry : 0u;
-            cur.state = d.next_state;
-            break;
+    // Software pipeline: the CTAs' partials of state n+1 are loaded (DSMEM)
+    // right after the barrier but folded only after the next face solve,
+    // which needs the cells and not dt; so is the run decision.
+    bool pending = false;  // partials loaded, not folded into cur yet
+    double pa = 0.0, pb = 0.0, ph = 0.0;
+    long long pbits = 0;
+    auto fold_partials = [&]() {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pa = smax(pa, __shfl_xor_sync(0xffffffffu, pa, o));
+            pb = smax(pb, __shfl_xor_sync(0xffffffffu, pb, o));
+            ph = smax(ph, __shfl_xor_sync(0xffffffffu, ph, o));
+            pbits |= __shfl_xor_sync(0xffffffffu, pbits, o);
         }
-        if (rank == 0 && t == 0 && C.fixed_dt <= 0 && C.dt_log && cur.steps < C.dt_cap)
-            C.dt_log[cur.steps] = d.dt;
+        cur.max_sx = pa > 0 ? (unsigned long long)__double_as_longlong(pa) : 0ull;
+        cur.max_sy = pb > 0 ? (unsigned long long)__double_as_longlong(pb) : 0ull;
+        cur.hmax = ph > 0 ? (unsigned long long)__double_as_longlong(ph) : 0ull;
+        cur.wet = (unsigned)(pbits & 1);
+        cur.err = (unsigned)(pbits >> 1);
+        pending = false;
+    };
+    for (int k = 0; k < n; ++k) {
         const int p = (int)(cur.steps & 1), q = p ^ 1;
         double c[4];
         if (ghost && bct == SILT_BC_GIVEN) {
@@ -956,8 +969,6 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
             for (int f = 0; f < 4; ++f) c[f] = src_cell[p][f * kF];
             if (ghost && bct != SILT_BC_PERIODIC) ghost_transform(A, side, c);
         }
-        const double c1 = d.dt / A.dx;
-        const double href = __longlong_as_double((long long)cur.hmax);
         Side sx;
         if constexpr (S) {
             sx = make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3]);
@@ -967,7 +978,19 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
         }
         const Side right = shfl_down_side(sx);
         Flux fx{0, 0, 0, 0, 0};
-        if (xface && !face_flux<S>(A.P, sx, right, fx)) {
+        const bool face_ok = !xface || face_flux<S>(A.P, sx, right, fx);
+        const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
+        const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
+        if (pending) fold_partials();
+        const RunDecision d = decide(A, cur);
+        if (!d.run) {  // what the remaining per-step launches would carry forward
+            cur.err |= (d.next_state == SILT_STATE_FAILED && !cur.err) ? kErrDry : 0u;
+            cur.state = d.next_state;
+            break;
+        }
+        if (rank == 0 && t == 0 && C.fixed_dt <= 0 && C.dt_log && cur.steps < C.dt_cap)
+            C.dt_log[cur.steps] = d.dt;
+        if (!face_ok) {
             errb |= kErrRiemann;
             if (atomicCAS(&A.ctl->err_claim, 0u, 1u) == 0u) {
                 A.ctl->err_bits = kErrRiemann;
@@ -977,8 +1000,8 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
                 for (int m = 0; m < 6; ++m) A.ctl->err_info[m] = info[m];
             }
         }
-        const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
-        const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
+        const double c1 = d.dt / A.dx;
+        const double href = __longlong_as_double((long long)cur.hmax);
         Reduce R{0.0, 0.0, 0.0, 0u};
         if (owned) {
             double o[4];
@@ -1042,34 +1065,24 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
             }
         }
         cl.sync();  // the new line and the CTA partials are visible cluster-wide
-        double a = 0.0, b = 0.0, h = 0.0;
-        long long bits = 0;
+        pa = pb = ph = 0.0;
+        pbits = 0;
         if (lane < nctas) {
             const double* rp = cl.map_shared_rank(&s_cta[q][0], lane);
-            a = rp[0];
-            b = rp[1];
-            h = rp[2];
-            bits = __double_as_longlong(rp[3]);
+            pa = rp[0];
+            pb = rp[1];
+            ph = rp[2];
+            pbits = __double_as_longlong(rp[3]);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            a = smax(a, __shfl_xor_sync(0xffffffffu, a, o));
-            b = smax(b, __shfl_xor_sync(0xffffffffu, b, o));
-            h = smax(h, __shfl_xor_sync(0xffffffffu, h, o));
-            bits |= __shfl_xor_sync(0xffffffffu, bits, o);
-        }
-        // the header of state n+1 (control_epilogue + reduce_flush of a launch)
+        pending = true;
+        // the run clock of state n+1 (control_epilogue); its reductions follow
         cur.t = d.t_new;
         cur.steps = cur.steps + 1;
         cur.last_dt = d.dt;
         cur.snap_idx = d.snap_idx;
         cur.state = d.next_state;
-        cur.max_sx = a > 0 ? (unsigned long long)__double_as_longlong(a) : 0ull;
-        cur.max_sy = b > 0 ? (unsigned long long)__double_as_longlong(b) : 0ull;
-        cur.hmax = h > 0 ? (unsigned long long)__double_as_longlong(h) : 0ull;
-        cur.wet = (unsigned)(bits & 1);
-        cur.err = (unsigned)(bits >> 1);
     }
+    if (pending) fold_partials();
     // state back to HBM (parity of its step count), header into the slot the
     // next launch reads, the one after it cleared for its reductions
     {
