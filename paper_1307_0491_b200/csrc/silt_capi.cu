@@ -447,7 +447,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     // rows per CTA: enough warps in flight for a fp64-latency-bound kernel
     const long long strips = (s->nx + kCellsPerWarp - 1) / kCellsPerWarp;
     long long R = (strips * s->ny + 16383) / 16384;  // C4s: 34, C4: 96 (capped), measured best
-    R = std::max(4LL, std::min(96LL, R));  // 96: measured best for C4 and Q
+    R = std::max(8LL, std::min(96LL, R));  // 96: measured best for C4 and Q; 8: C3 (+8 % over 4)
     if (R >= 32) R -= R % 16;              // C5: 64 (not 69), C4s: 32
     if (const char* e = std::getenv("SILT_ROWS")) R = std::max(1LL, std::atoll(e));
     if (problem->dim == 1) R = 1;
