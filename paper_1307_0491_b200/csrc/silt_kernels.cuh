@@ -924,7 +924,8 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
     const int bct = ghost ? A.bc_type[side] : SILT_BC_OUTFLOW;
     if (ghost) src = (bct == SILT_BC_PERIODIC) ? (col < 0 ? nx - 1 : 0) : (col < 0 ? 0 : nx - 1);
     const int owner = src / kCluster1dCells, idx = src - owner * kCluster1dCells;
-    double* const own_cell[2] = {&s_line[0][0][col - base], &s_line[1][0][col - base]};
+    const int oi = owned ? col - base : 0;  // this lane's slot in the CTA's line
+    double* const own_cell[2] = {&s_line[0][0][oi], &s_line[1][0][oi]};
     double* const src_cell[2] = {cl.map_shared_rank(&s_line[0][0][idx], owner),
                                  cl.map_shared_rank(&s_line[1][0][idx], owner)};
     constexpr int kF = kCluster1dCells;  // field stride in s_line
