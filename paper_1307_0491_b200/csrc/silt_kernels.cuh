@@ -1222,10 +1222,8 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
     int NAME##_step1d_cluster(const StepArgs& A, int li0, int n, int ctas, cudaStream_t st) {    \
         StepArgs a = A;                                                                          \
         void* args[] = {&a, &li0, &n};                                                           \
-        static const int resident_env = [] {                                                     \
-            const char* e = std::getenv("SILT_1D_RESIDENT");                                     \
-            return e ? std::atoi(e) : -1;                                                        \
-        }();                                                                                     \
+        const char* renv = std::getenv("SILT_1D_RESIDENT"); /* per launch: tests switch it */   \
+        const int resident_env = renv ? std::atoi(renv) : -1;                                    \
         const bool resident = resident_env >= 0 ? resident_env != 0 : ctas <= silt_dev::kResidentMaxCtas; \
         const void* f =                                                                          \
             resident ? (A.P.shields ? (const void*)silt_dev::step1d_resident_kernel<S, true>     \

@@ -516,3 +516,27 @@ def test_streak_loop_is_bit_identical(N, monkeypatch, bcs):
         strips = g.gather()
         g.close()
         assert np.array_equal(strips, ref[0])
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "periodic_ring1d"])
+@pytest.mark.parametrize("resident", ["0", "1"])
+def test_1d_cluster_kernels(N, golden, monkeypatch, case, resident):
+    """Both multi-step 1D cluster kernels — the line resident in shared memory
+    (DSMEM halo cells and reductions) and the global-memory one — reproduce
+    the reference's fixtures bit for bit (STRICT) and within the bars (FAST)."""
+    data, meta = golden
+    m = meta["cases"][case]
+    p = problem_from_meta(m)
+    t_end = math.inf if m["t_end"] is None else m["t_end"]
+    monkeypatch.setenv("SILT_1D_RESIDENT", resident)
+    ref, ref_log = data[f"{case}_final"], data[f"{case}_dt"]
+    out, t, n, log = N.run(p, data[f"{case}_init"], t_end=t_end, max_steps=m["max_steps"],
+                           snapshots=m["snapshots"], variant=abi.VARIANT_STRICT)
+    assert n == m["steps"] and t == m["t_final"]
+    assert np.array_equal(log, ref_log)
+    assert np.array_equal(out, ref)
+    fo, ft, fn, flog = N.run(p, data[f"{case}_init"], t_end=t_end, max_steps=m["max_steps"],
+                             snapshots=m["snapshots"], variant=abi.VARIANT_FAST)
+    assert fn == n
+    assert np.max(np.abs(flog - ref_log) / ref_log) <= DT_TOL
+    assert np.all(normwise(fo, ref) <= FIELD_TOL)
