@@ -5,13 +5,16 @@
 //
 // K1 step2d: one launch per time step.  Each warp owns a column strip of 30
 // cells and marches up R rows.  Lane l holds column i0-1+l: lanes 1..30 own
-// cells, lanes 0 and 31 are the x-halo.  Per row:
-//   load state n (SoA, coalesced fp64) -> per-cell relaxation terms for the
-//   x and y axes (computed once, shared by both faces of the cell) ->
-//   x-face problem (right neighbour's terms by warp shuffle) -> x update ->
-//   y-face problem against the previous row (kept in shared memory) -> y
-//   update of the previous row -> check_depth -> store state n+1 -> CFL/hmax
-//   candidates of state n+1 (the NEXT step's cfl_dt) folded into registers.
+// cells, lanes 0 and 31 are the x-halo.  Rows of state n arrive through a
+// cp.async ring in shared memory (RING-1 rows in flight).  Per row:
+//   per-cell relaxation terms for the x and y axes (computed once, shared by
+//   both faces of the cell) -> y-face problem against the previous row (its
+//   terms parked in shared memory) -> y update of the previous row ->
+//   check_depth -> store state n+1 -> CFL/hmax candidates of state n+1 (the
+//   NEXT step's cfl_dt) folded into registers -> x-face problem (right
+//   neighbour's terms from shared memory) -> x update parked for the next row.
+// Quiescent rows (FAST) are stored unchanged without any face solve, and a
+// streak of them runs in a short inner loop (load, compare, vote, store).
 // Every face is solved exactly once per launch: x faces by the lane left of
 // them (the halo lanes 0 and 31 make each x face belong to exactly one warp),
 // y faces by the owning column, so depth and bed updates telescope exactly.
