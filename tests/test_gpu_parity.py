@@ -385,6 +385,41 @@ def test_c5_1000_steps_fast_vs_strict(N):
     assert max(err) <= FIELD_TOL and mom <= FIELD_TOL
 
 
+def test_c5_full_size_fast_vs_strict(N):
+    """BASELINE config 5 at its stated size and length on one GPU: the
+    32768 x 8192 random bed (the 8-GPU stress test's whole grid), 300 steps,
+    FAST against STRICT: identical step count, dt within 1e-12, fields within
+    1e-9 normwise (hv against the momentum scale)."""
+    import torch
+
+    import bench
+    p = bench.build_global_problem("C5", 8)
+    assert (p.ny, p.nx) == (32768, 8192)
+    init = bench.device_initial_rows("C5", p, 0, p.ny, torch.device("cuda"))
+    steps = 300
+    outs, logs = [], []
+    for variant in (abi.VARIANT_FAST, abi.VARIANT_STRICT):
+        s = N.Solver(p, variant=variant)
+        torch.cuda.synchronize()
+        s.upload_device(init.data_ptr())
+        s.begin(max_steps=steps, dt_cap=steps)
+        st = s.run(batch=50)
+        assert st.steps == steps
+        out = torch.empty_like(init)
+        s.download_device(out.data_ptr())
+        logs.append(s.dt_log(steps))
+        s.close()
+        outs.append(out)
+        torch.cuda.synchronize()
+    fo, so = outs
+    assert np.max(np.abs(logs[0] - logs[1]) / logs[1]) <= DT_TOL
+    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in (0, 1, 3)]
+    mom = float((fo[..., 2] - so[..., 2]).abs().max() /
+                torch.maximum(so[..., 1].abs().max(), so[..., 2].abs().max()))
+    print("C5 full size 300 steps fast vs strict: h, hu, zb", err, "hv/momentum", mom)
+    assert max(err) <= FIELD_TOL and mom <= FIELD_TOL
+
+
 @pytest.mark.slow
 def test_c5_size_properties(N):
     """C5 random bed at the per-GPU weak-scaling size (8192 x 4096 rows),
