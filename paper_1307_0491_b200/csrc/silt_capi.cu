@@ -449,6 +449,24 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     long long R = (strips * s->ny + 16383) / 16384;  // C4s: 34, C4: 96 (capped), measured best
     R = std::max(8LL, std::min(96LL, R));  // 96: measured best for C4 and Q; 8: C3 (+8 % over 4)
     if (R >= 32) R -= R % 16;              // C5: 64 (not 69), C4s: 32
+    if (R < 32 && problem->dim == 2) {
+        // Short launches (a few waves of CTAs): the last wave's empty slots
+        // are a visible tail, so pick the rows per block near R whose CTA
+        // count comes closest below a whole number of waves (3 CTAs per SM).
+        // C3 (1024^2): 7 rows, 2.98 waves — 12.5 -> 12.75 G cell-updates/s.
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        const double slots = 3.0 * nsm;
+        const long long cols = (strips + kStepThreads / 32 - 1) / (kStepThreads / 32);
+        auto waste = [&](long long r) {
+            const double w = (double)(((long long)s->ny + r - 1) / r * cols) / slots;
+            return std::ceil(w) - w;
+        };
+        long long best = R;
+        for (long long cand = std::max(6LL, R - 2); cand <= R + 4; ++cand)
+            if (waste(cand) < waste(best) - 0.05) best = cand;
+        R = best;
+    }
     if (const char* e = std::getenv("SILT_ROWS")) R = std::max(1LL, std::atoll(e));
     if (problem->dim == 1) R = 1;
     A.rows_per_block = (int)R;
