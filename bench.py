@@ -423,7 +423,10 @@ def main():
                        "law": args.law, "nx": p.nx, "ny": p.ny, "rows_per_gpu": nrows,
                        "parallelism": f"row strips x{world}",
                        "partition": (args.partition if world > 1 else "single strip"),
-                       "l2": "state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells},
+                       "l2": ("state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells
+                              if 64 * cells > 4 * 126e6 else
+                              "state 64 B/cell x %d cells is L2-sized; not flushed (a step re-reads "
+                              "the previous step's output: L2-resident by design)" % cells)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
