@@ -278,6 +278,13 @@ int check_cfl(double cfl) {
     return SILT_OK;
 }
 
+#ifndef SILT_WAVE_R
+#define SILT_WAVE_R 48
+#endif
+#ifndef SILT_WAVE_DOWN
+#define SILT_WAVE_DOWN 8
+#endif
+
 // part 0: the whole step; 1: the two boundary row blocks of a split step;
 // 2: its interior row blocks (and the end of the step).
 void launch_step(silt_solver* s, int part = 0) {
@@ -449,7 +456,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     long long R = (strips * s->ny + 16383) / 16384;  // C4s: 34, C4: 96 (capped), measured best
     R = std::max(8LL, std::min(96LL, R));  // 96: measured best for C4 and Q; 8: C3 (+8 % over 4)
     if (R >= 32) R -= R % 16;              // C5: 64 (not 69), C4s: 32
-    if (R < 32 && problem->dim == 2) {
+    if (R < SILT_WAVE_R && problem->dim == 2) {
         // Short launches (a few waves of CTAs): the last wave's empty slots
         // are a visible tail, so pick the rows per block near R whose CTA
         // count comes closest below a whole number of waves (3 CTAs per SM).
@@ -463,7 +470,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
             return std::ceil(w) - w;
         };
         long long best = R;
-        for (long long cand = std::max(6LL, R - 2); cand <= R + 4; ++cand)
+        for (long long cand = std::max(6LL, R - SILT_WAVE_DOWN); cand <= R + 4; ++cand)
             if (waste(cand) < waste(best) - 0.05) best = cand;
         R = best;
     }
