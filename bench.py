@@ -143,84 +143,148 @@ def device_initial_rows(wl: str, p, j0: int, nrows: int, device):
         out[..., 1] = 10.0
         out[..., 3] = zb
     else:
-        # random bed generated per strip on the host (counter-based, seeded)
-        _, init, _ = S.random_bed_2d(nx, p.ny, a_g=p.a_g, cfl=p.cfl) if p.ny * nx <= (1 << 26) \
-            else (None, None, None)
-        if init is None:
-            g = torch.Generator(device=device)
-            g.manual_seed(1307 + j0)
-            noise = torch.randn((nrows, nx), generator=g, device=device, dtype=torch.float64)
-            kx = torch.fft.rfftfreq(nx, device=device, dtype=torch.float64)
-            ky = torch.fft.fftfreq(nrows, device=device, dtype=torch.float64)
-            filt = torch.exp(-2.0 * (math.pi * 20.0) ** 2 * (ky[:, None] ** 2 + kx[None, :] ** 2))
-            grf = torch.fft.irfft2(torch.fft.rfft2(noise) * filt, s=(nrows, nx))
-            grf = (grf - grf.mean()) / grf.std()
-            zb = 0.1 + 0.05 * grf.clamp(-1.0, 1.0)
-            out[..., 0] = 2.0 - zb
-            out[..., 1] = 0.5 + torch.rand((nrows, nx), generator=g, device=device, dtype=torch.float64)
-            out[..., 2] = -0.1 + 0.2 * torch.rand((nrows, nx), generator=g, device=device,
-                                                  dtype=torch.float64)
-            out[..., 3] = zb
-        else:
-            out.copy_(torch.from_numpy(init[j0:j0 + nrows]))
+        # C5: the seeded 8192 x 4096 tile (scenarios.random_bed_2d; periodic
+        # Gaussian random field) repeated along y, so the global field is the
+        # same for every GPU count and N = 1 is exactly the reference-pinned
+        # tile (tests/test_gpu_big.py)
+        tile = c5_tile(nx)
+        rows = (np.arange(j0, j0 + nrows) % tile.shape[0])
+        out.copy_(torch.from_numpy(np.ascontiguousarray(tile[rows])))
     return out
 
 
-_SAMPLES: dict = {}
+_TILES: dict = {}
 
 
-def _reference_sample_input(wl: str, law: str):
-    """(problem, initial rows, description) of the bounded CPU sample, built once."""
-    key = (wl, law)
-    if key in _SAMPLES:
-        return _SAMPLES[key]
-    import numpy as np
-    from paper_1307_0491_b200 import abi, scenarios as S
+def c5_tile(nx: int):
+    """The C5 random-bed tile (nx x ny_per_gpu, BASELINE configs[4] per GPU)."""
+    from paper_1307_0491_b200 import scenarios as S
+    if nx not in _TILES:
+        w = WORKLOADS["C5"]
+        _, _TILES[nx], _ = S.random_bed_2d(nx, w["ny_per_gpu"], a_g=w["a_g"], cfl=w["cfl"])
+    return _TILES[nx]
+
+
+def cpu_model() -> str:
+    """Host CPU model (for the CPU-baseline report)."""
+    name, fam, model = "unknown", "?", "?"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name" and name == "unknown":
+                    name = v
+                elif k == "cpu family" and fam == "?":
+                    fam = v
+                elif k == "model" and model == "?":
+                    model = v
+    except OSError:
+        pass
+    return f"{name} (family {fam} model {model}), {os.cpu_count()} logical CPUs"
+
+
+def host_workload(wl: str, world: int, law: str = "grass"):
+    """(problem, AoS initial field) of the whole workload on the host — the
+    same grid, law and initial data our arm uploads (bitwise: the device
+    builder of device_initial_rows restates these constructions)."""
+    from paper_1307_0491_b200 import scenarios as S
     w = WORKLOADS[wl]
+    p = build_global_problem(wl, world, law)
     if w["kind"] == "dune":
+        _, init, _ = S.dune_2d(w["n"])
+    elif w["kind"] == "uniform":
+        import numpy as np
+        init = np.zeros((p.ny, p.nx, 4))
+        init[..., 0] = 9.9
+        init[..., 1] = 10.0
+        init[..., 3] = 0.1
+    else:
+        import numpy as np
+        tile = c5_tile(w["nx"])
+        init = np.ascontiguousarray(tile[np.arange(p.ny) % tile.shape[0]])
+    return p, init
+
+
+def cpu_reference_window(wl: str, world: int, steps_lo: int, steps_hi: int, threads: int,
+                         law: str = "grass"):
+    """The reference's own CPU driver, silt::run_parallel(sc, 1, P) (oracle/_ref,
+    the unmodified reference core), on the WHOLE workload grid: cell-updates/s
+    over steps [steps_lo, steps_hi) from t = 0, timed by the reference's own
+    WorkerTiming.compute_seconds (src/parallel.cpp:318-361; max over workers):
+    one run of steps_hi steps minus one of steps_lo steps."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    p, init = host_workload(wl, world, law)
+    if O.have_reference():
+        R, kind = O.reference(), "reference"
+    else:  # the GPU box always has the prebuilt oracle/_ref; the port is the fallback
+        R, kind, threads = O.restatement(), "port", 1
+    P = max(1, min(threads, p.ny))
+
+    def compute(n):
+        if n <= 0:
+            return 0.0, 0
+        if kind == "reference":
+            _, _, ns, comp, _ = R.run_parallel(p, init, 1, P, max_steps=n, want_field=False)
+            return comp, ns
+        t0 = time.perf_counter()
+        _, _, ns, _ = R.run(p, init, max_steps=n, dt_log=False)
+        return time.perf_counter() - t0, ns
+
+    c_lo, n_lo = compute(steps_lo)
+    c_hi, n_hi = compute(steps_hi)
+    assert n_hi - n_lo == steps_hi - steps_lo
+    rate = p.nx * p.ny * (n_hi - n_lo) / (c_hi - c_lo)
+    desc = (f"{wl} whole grid {p.nx}x{p.ny}, steps [{steps_lo}, {steps_hi}) from t=0, "
+            f"run_parallel(sc, 1, {P}), WorkerTiming.compute_seconds")
+    return rate, desc, kind, P
+
+
+def cpu_reference_band_p1(wl: str, law: str = "grass"):
+    """Single-thread reference rate, run_parallel(sc, 1, 1), on a 96-row band of
+    the workload (the whole grid at P = 1 would take minutes per step)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.have_reference():
+        return None
+    from paper_1307_0491_b200 import abi
+    p_full, init_full = host_workload(wl, 1, law) if WORKLOADS[wl].get("n", 0) <= 4096 \
+        else (None, None)
+    w = WORKLOADS[wl]
+    if p_full is None:  # a C4-sized dune: build only the band
+        from paper_1307_0491_b200 import scenarios as S
         n = w["n"]
-        rows = 96 if n >= 8192 else min(n, 256)
-        # a band of C4/C3 rows through the mound (y in [400, 600] m)
+        rows = 96
         j0 = int(0.45 * n)
-        p_full = abi.make_problem(2, n, n, 1000.0 / n, 1000.0 / n, a_g=w["a_g"], cfl=w["cfl"])
-        wx = S._sine_bump(S._centres(n, p_full.dx), 300.0, 200.0)
-        wy = S._sine_bump(S._centres(n, p_full.dy), 400.0, 200.0)[j0:j0 + rows]
+        dx = 1000.0 / n
+        wx = S._sine_bump(S._centres(n, dx), 300.0, 200.0)
+        wy = S._sine_bump(S._centres(n, dx), 400.0, 200.0)[j0:j0 + rows]
         init = np.zeros((rows, n, 4))
         zb = 0.1 + np.multiply.outer(wy, wx)
         init[..., 0] = 10.0 - zb
         init[..., 1] = 10.0
         init[..., 3] = zb
-        p = abi.make_problem(2, n, rows, p_full.dx, p_full.dy, a_g=w["a_g"], cfl=w["cfl"])
-        desc = f"{wl} rows [{j0},{j0 + rows}) x {n} cols"
+        p = abi.make_problem(2, n, rows, dx, dx, a_g=w["a_g"], cfl=w["cfl"])
+        apply_law(p, law)
+        desc = f"rows [{j0},{j0 + rows}) x {n}, 1 step"
     else:
-        p, init, _ = S.random_bed_2d(w["nx"], 64, a_g=w["a_g"], cfl=w["cfl"])
-        desc = f"{wl} {w['nx']} x 64 rows"
-    apply_law(p, law)
-    _SAMPLES[key] = (p, init, desc)
-    return _SAMPLES[key]
+        rows = min(96, p_full.ny)
+        init = np.ascontiguousarray(init_full[:rows])
+        p = abi.make_problem(2, p_full.nx, rows, p_full.dx, p_full.dy, a_g=p_full.a_g,
+                             cfl=p_full.cfl)
+        apply_law(p, law)
+        desc = f"rows [0,{rows}) x {p.nx}, 1 step"
+    _, _, ns, comp, _ = O.reference().run_parallel(p, init, 1, 1, max_steps=1, want_field=False)
+    return {"value": p.nx * p.ny * ns / comp, "unit": "cell-updates/s", "cores": 1,
+            "sample": desc}
 
 
-def cpu_reference_sample(wl: str, steps: int, threads: int, law: str = "grass"):
-    """The reference's CPU run_parallel (oracle/_ref) on a bounded row sample
-    of the workload; returns (cell-updates/s, description)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    p, init, desc = _reference_sample_input(wl, law)
-    R = O.reference() if O.have_reference() else None
-    kind = "reference"
-    if R is None:
-        R, kind = O.restatement(), "port"
-    t0 = time.perf_counter()
-    if kind == "reference":
-        _, _, n_steps, comp, _ = R.run_parallel(p, init, 1, min(threads, p.ny),
-                                                max_steps=steps, want_field=False)
-        secs = comp
-    else:
-        _, _, n_steps, _ = R.run(p, init, max_steps=steps)
-        secs = time.perf_counter() - t0
-        threads = 1
-    cells = p.nx * p.ny * n_steps
-    return cells / secs, f"{desc}, {n_steps} steps", kind, threads
+def workload_config(args, p) -> dict:
+    """The workload both arms run (identical dicts: the driver compares them)."""
+    return {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
+            "law": args.law, "nx": p.nx, "ny": p.ny}
 
 
 def run_reference_arm(args):
@@ -228,14 +292,9 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    total_cells = 0.0
-    total_secs = 0.0
-    for s in range(args.warmup + args.steps):
-        rate, desc, kind, used = cpu_reference_sample(args.workload, 1, threads, args.law)
-        if s >= args.warmup:
-            total_secs += 1.0 / rate
-            total_cells += 1.0
-    value = total_cells / total_secs
+    lo, hi = args.warmup, args.warmup + args.steps
+    value, desc, kind, used = cpu_reference_window(args.workload, args.gpus, lo, hi, threads,
+                                                   args.law)
     p = build_global_problem(args.workload, args.gpus, args.law)
     line = {
         "metric": "cell-updates/s (fp64, 2D)", "value": value, "unit": "cell-updates/s",
@@ -243,11 +302,12 @@ def run_reference_arm(args):
         "higher_is_better": True,
         "scaling": "weak" if WORKLOADS[args.workload]["kind"] == "random" else "strong",
         "dtype": "f64", "data": "synthetic",
-        # the same workload string as our arm's line; the reference runs a bounded sample of it
-        "config": {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
-                   "law": args.law, "nx": p.nx, "ny": p.ny,
-                   "parallelism": f"reference run_parallel(sc, 1, {used}) on host threads",
-                   "sample": desc},
+        "config": workload_config(args, p),
+        "reference_run": {"driver": f"silt::run_parallel(sc, 1, {used}) (oracle/_ref)",
+                          "timing": f"compute_seconds(run of {hi} steps) - compute_seconds(run "
+                                    f"of {lo} steps): the {args.steps} steps after {lo} "
+                                    "warm-up steps",
+                          "cpu": cpu_model(), "threads": used},
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": used, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
@@ -397,9 +457,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, desc, kind, used = cpu_reference_sample(args.workload, 3, os.cpu_count() or 1, args.law)
+            rate, desc, kind, used = cpu_reference_window(args.workload, 1, 0, 2,
+                                                          os.cpu_count() or 1, args.law)
             cpu = {"value": rate, "unit": "cell-updates/s", "cores": used, "kind": kind,
-                   "sample": desc}
+                   "sample": desc, "cpu": cpu_model()}
+            if args.workload in ("C3", "C4", "C4s"):
+                cpu["p1"] = cpu_reference_band_p1(args.workload, args.law)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -419,9 +482,8 @@ def main():
             "dtype": "f64",
             "data": "synthetic",
             "variant": args.variant,
-            "config": {"workload": f"{args.workload} ({p.nx}x{p.ny}, A_g={p.a_g}, CFL={p.cfl})",
-                       "law": args.law, "nx": p.nx, "ny": p.ny, "rows_per_gpu": nrows,
-                       "parallelism": f"row strips x{world}",
+            "config": workload_config(args, p),
+            "layout": {"rows_per_gpu": nrows, "parallelism": f"row strips x{world}",
                        "partition": (args.partition if world > 1 else "single strip"),
                        "l2": ("state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells
                               if 64 * cells > 4 * 126e6 else
@@ -430,7 +492,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
-                         "note": "algorithmic 64 B/cell-update / step-kernel duration"},
+                         "note": "algorithmic 64 B/cell-update / device time per step (the step "
+                                 "kernel plus, in launches >= 64 CTAs/SM, the 1-CTA "
+                                 "rb_order_kernel that orders the next launch, ~0.1 %)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

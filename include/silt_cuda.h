@@ -8,7 +8,7 @@
  * passed as `void*` holding a cudaStream_t).  Each function returns a status
  * code (SILT_OK == 0); the message of the last failure on the calling thread
  * is available from silt_last_error().  The C++ shim
- * (paper_1307_0491_b200/csrc/silt_api.hpp) maps the codes back onto the
+ * (paper_1307_0491_b200/csrc/silt_gpu.hpp) maps the codes back onto the
  * reference's exception types.
  *
  * Reference interfaces replaced (paths relative to the reference checkout

@@ -95,6 +95,10 @@ class CpuSolver:
             g.argtypes = [_P, _D, C.c_double, _I64, C.c_int, C.c_int, _D,
                           C.POINTER(_I64), _D, _D, _D]
             self._runp = g
+            g = L.ref_run_blocks
+            g.argtypes = [_P, _D, _I64, C.c_int, C.c_int, _D, _D, C.POINTER(_I64), _D]
+            g.restype = C.c_int
+            self._runb = g
 
     def _check(self, rc: int):
         if rc != 0:
@@ -128,6 +132,19 @@ class CpuSolver:
                                int(px), int(py), _dp(out) if want_field else None,
                                C.byref(steps), C.byref(t), C.byref(comp), C.byref(wall)))
         return out, t.value, steps.value, comp.value, wall.value
+
+    def run_blocks(self, problem, init, max_steps: int, py: int, threads: int):
+        """run_parallel's loop on Topology{1, py} through the public API with a
+        dt log (ref_run_blocks): (field, t, steps, dt_log)."""
+        init = np.ascontiguousarray(init, dtype=np.float64)
+        out = np.empty_like(init)
+        log = np.zeros(max(int(max_steps), 1))
+        steps = _I64(0)
+        t = C.c_double(0)
+        self._check(self._runb(C.byref(problem), _dp(init), int(max_steps), int(py),
+                               int(threads), _dp(out), _dp(log), C.byref(steps),
+                               C.byref(t)))
+        return out, t.value, steps.value, log[:steps.value].copy()
 
     def cfl_dt(self, problem, field) -> float:
         field = np.ascontiguousarray(field, dtype=np.float64)

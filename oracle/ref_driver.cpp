@@ -24,6 +24,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "silt/io.hpp"
@@ -201,6 +202,62 @@ int ref_run_parallel(const silt_problem* p, const double* init, double t_end,
         for (const WorkerTiming& w : r.timing) cmax = std::max(cmax, w.compute_seconds);
         if (compute_seconds) *compute_seconds = cmax;
         if (wall_seconds) *wall_seconds = r.wall_seconds;
+    });
+}
+
+// run_parallel's step loop (src/parallel.cpp:315-364) for Topology{1, py},
+// re-expressed through the public API so the dt sequence can be logged:
+// halo_exchange + apply_bc_side on the physical sides, cfl_dt per block,
+// global_dt, step_2d per block — the blocks' phases on `threads` host
+// threads.  No snapshots, t_end = inf; every BC must be non-periodic.  Used
+// to generate the large-grid fixtures (tests/golden/make_golden_big.py).
+int ref_run_blocks(const silt_problem* p, const double* init, int64_t max_steps, int py,
+                   int threads, double* out, double* dt_log, int64_t* steps_out,
+                   double* t_out) {
+    return guarded([&] {
+        const Scenario sc = make_scenario(*p, init, std::numeric_limits<double>::infinity());
+        for (int s = 0; s < 4; ++s)
+            if (sc.bc[s].type == BcType::Periodic)
+                throw std::invalid_argument("ref_run_blocks: periodic sides not supported");
+        Topology topo;
+        topo.px = 1;
+        topo.py = py;
+        std::vector<Subdomain> parts = partition(sc.initial, topo);
+        std::vector<double> locals(parts.size());
+        auto each = [&](auto&& fn) {
+            std::vector<std::thread> pool;
+            const int nt = std::max(1, std::min<int>(threads, (int)parts.size()));
+            for (int w = 0; w < nt; ++w)
+                pool.emplace_back([&, w] {
+                    for (std::size_t k = w; k < parts.size(); k += nt) fn(k);
+                });
+            for (auto& th : pool) th.join();
+        };
+        double t = 0;
+        int64_t steps = 0;
+        while (max_steps < 0 || steps < max_steps) {
+            halo_exchange(parts, topo, false);
+            each([&](std::size_t k) {
+                Subdomain& sd = parts[k];
+                apply_bc_side(sd.field, Side::West, sc.bc[0]);
+                apply_bc_side(sd.field, Side::East, sc.bc[1]);
+                if (topo.neighbor(sd.rank, 0, -1) < 0)
+                    apply_bc_side(sd.field, Side::South, sc.bc[2]);
+                if (topo.neighbor(sd.rank, 0, +1) < 0)
+                    apply_bc_side(sd.field, Side::North, sc.bc[3]);
+                locals[k] = cfl_dt(sd.field, sc.law, sc.phys, sc.cfl);
+            });
+            const double dt = global_dt(locals);
+            each([&](std::size_t k) {
+                step_2d(parts[k].field, sc.law, sc.phys, dt, sc.safety);
+            });
+            if (dt_log) dt_log[steps] = dt;
+            t = t + dt;
+            ++steps;
+        }
+        store_field(gather(parts, topo, sc.grid), out);
+        *steps_out = steps;
+        *t_out = t;
     });
 }
 

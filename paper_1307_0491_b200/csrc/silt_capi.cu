@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -182,6 +183,7 @@ struct silt_solver {
     cudaEvent_t cap_ready = nullptr, cap_done = nullptr;
     bool cap_pending = false;
     std::thread writer;         // asynchronous CSV snapshot (silt_solver_capture_write)
+    std::atomic<bool> writer_busy{false};  // set by capture_write, cleared by the thread
     int writer_rc = SILT_OK;
     std::string writer_err;
     Control* ctl = nullptr;
@@ -451,6 +453,15 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
     A.ghost_w = s->cols;
     A.ghost_e = s->cols + 4 * (size_t)s->ny;
     A.ctl = s->ctl;
+    // resident step CTAs per SM of this variant and law (occupancy of the
+    // 2D kernel with its dynamic shared memory; 3 for both variants today)
+    int ctas_per_sm = 3;
+    if (problem->dim == 2) {
+        const int q = variant == SILT_VARIANT_STRICT
+                          ? silt_strict_step2d_ctas_per_sm(problem->law_kind == SILT_LAW_SHIELDS)
+                          : silt_fast_step2d_ctas_per_sm(problem->law_kind == SILT_LAW_SHIELDS);
+        if (q > 0) ctas_per_sm = q;
+    }
     // rows per CTA: enough warps in flight for a fp64-latency-bound kernel
     const long long strips = (s->nx + kCellsPerWarp - 1) / kCellsPerWarp;
     long long R = (strips * s->ny + 16383) / 16384;  // C4s: 34, C4: 96 (capped), measured best
@@ -464,7 +475,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         // C4s (4096^2): 25 rows, 12.9 waves — 0.263 -> 0.257 ms per step.
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-        const double slots = 3.0 * nsm;
+        const double slots = (double)ctas_per_sm * nsm;
         const long long cols = (strips + kStepThreads / 32 - 1) / (kStepThreads / 32);
         auto waste = [&](long long r) {
             const double w = (double)(((long long)s->ny + r - 1) / r * cols) / slots;
@@ -513,7 +524,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         // 1 - 6.5 / waves: C4 on one GPU (53 waves) 0.88, its 2-strip halves
         // (26 waves) 0.75 — measured best 0.85-0.90 and 0.60-0.75.
         {
-            const double waves = (double)ctas / (3.0 * sms);
+            const double waves = (double)ctas / ((double)ctas_per_sm * sms);
             s->rb_span = (int)std::max(500.0, std::min(900.0, 1000.0 * (1.0 - 6.5 / waves)));
         }
         if (const char* es = std::getenv("SILT_RB_SPAN")) s->rb_span = std::max(100, std::min(1000, std::atoi(es)));
@@ -670,6 +681,13 @@ int silt_solver_capture_wait(silt_solver* s) {
 int silt_solver_capture_query(silt_solver* s, int* landed) {
     if (!s || !landed) return fail(SILT_ERR_INVALID, "silt_solver_capture_query: null argument");
     *landed = 1;
+    if (s->writer.joinable()) {  // an asynchronous CSV snapshot: landed once written
+        if (s->writer_busy.load(std::memory_order_acquire)) {
+            *landed = 0;
+            return SILT_OK;
+        }
+        return silt_solver_capture_wait(s);  // joins, reports the writer's error
+    }
     if (!s->cap_pending) return SILT_OK;
     CUDA_TRY(cudaSetDevice(s->device));
     const cudaError_t e = cudaEventQuery(s->cap_done);
@@ -773,6 +791,21 @@ int silt_solver_begin(silt_solver* s, const silt_run_plan* plan) {
     std::sort(snaps.begin(), snaps.end());
     snaps.erase(std::unique(snaps.begin(), snaps.end()), snaps.end());
     CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (s->begun) {
+        // A new run from the current state: the run clock restarts at parity
+        // 0, so after an odd number of steps state n lives in plane set 1 and
+        // is moved to plane set 0 first (otherwise the run would restart one
+        // step stale).
+        if (int rc = silt_solver_capture_wait(s)) return rc;
+        Slot sl;
+        if (int rc = read_slot(s, &sl, nullptr)) return rc;
+        if (sl.steps & 1) {
+            const size_t bytes = (size_t)s->ny * s->pitch * sizeof(double);
+            for (int f = 0; f < 4; ++f)
+                CUDA_TRY(cudaMemcpyAsync(s->args.state[0][f], s->args.state[1][f], bytes,
+                                         cudaMemcpyDeviceToDevice, s->stream));
+        }
+    }
     if ((int)snaps.size() > s->n_snaps_alloc) {
         cudaFree(s->snaps);
         s->snaps = nullptr;
@@ -794,6 +827,7 @@ int silt_solver_begin(silt_solver* s, const silt_run_plan* plan) {
     c.t_end = plan->t_end;
     c.max_steps = plan->max_steps;
     c.fixed_dt = 0;
+    c.fixed_mode = 0;
     c.dt_cap = std::min<int64_t>(plan->dt_log_capacity, s->dt_cap);
     c.dt_log = s->dt_log;
     c.snaps = s->snaps;
@@ -891,13 +925,22 @@ int silt_solver_step_fixed(silt_solver* s, double dt) {
     if (!s) return fail(SILT_ERR_INVALID, "null solver");
     if (!s->begun) return fail(SILT_ERR_INVALID, "silt_solver_step_fixed: call begin first");
     CUDA_TRY(cudaSetDevice(s->device));
+    // the caller's dt is applied exactly as given, like step_1d/step_2d
+    // (src/stepper.cpp:118-189): 0 leaves the field unchanged, a NaN makes
+    // check_depth fail ("negative depth produced"), as in the reference
     s->host_ctl->fixed_dt = dt;
+    s->host_ctl->fixed_mode = 1;
     CUDA_TRY(cudaMemcpyAsync(&s->ctl->fixed_dt, &s->host_ctl->fixed_dt, sizeof(double),
+                             cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(&s->ctl->fixed_mode, &s->host_ctl->fixed_mode, sizeof(int),
                              cudaMemcpyHostToDevice, s->stream));
     launch_step(s);
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     s->host_ctl->fixed_dt = 0;
+    s->host_ctl->fixed_mode = 0;
     CUDA_TRY(cudaMemcpy(&s->ctl->fixed_dt, &s->host_ctl->fixed_dt, sizeof(double),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(&s->ctl->fixed_mode, &s->host_ctl->fixed_mode, sizeof(int),
                         cudaMemcpyHostToDevice));
     CUDA_TRY(cudaGetLastError());
     return SILT_OK;
@@ -1842,6 +1885,7 @@ extern "C" int silt_solver_capture_write(silt_solver* s, double time, const char
     CUDA_TRY(cudaMemcpy(&slot->state, &st, sizeof(int), cudaMemcpyHostToDevice));
     const std::string file(path);
     s->writer_rc = SILT_OK;
+    s->writer_busy.store(true, std::memory_order_relaxed);
     s->writer = std::thread([s, time, file, append] {
         cudaSetDevice(s->device);
         if (cudaEventSynchronize(s->cap_ready) != cudaSuccess) {
@@ -1858,6 +1902,7 @@ extern "C" int silt_solver_capture_write(silt_solver* s, double time, const char
         }
         s->writer_rc = rc;
         if (rc != SILT_OK) s->writer_err = silt_last_error();
+        s->writer_busy.store(false, std::memory_order_release);
     });
     return SILT_OK;
 }

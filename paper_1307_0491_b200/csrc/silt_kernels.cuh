@@ -82,7 +82,7 @@ __device__ __forceinline__ RunDecision decide(const StepArgs& A, const Slot& cur
         d.next_state = SILT_STATE_FAILED;
         return d;
     }
-    if (C.fixed_dt > 0) {
+    if (C.fixed_mode) {  // step_1d/step_2d(f, ..., dt): any dt, as given
         d.run = true;
         d.dt = C.fixed_dt;
         d.t_new = cur.t + d.dt;
@@ -133,7 +133,7 @@ __device__ __forceinline__ void control_epilogue(const StepArgs& A, int li, cons
         nxt.last_dt = d.dt;
         nxt.snap_idx = d.snap_idx;
         nxt.state = d.next_state;
-        if (C.fixed_dt <= 0 && C.dt_log && cur.steps < C.dt_cap) C.dt_log[cur.steps] = d.dt;
+        if (!C.fixed_mode && C.dt_log && cur.steps < C.dt_cap) C.dt_log[cur.steps] = d.dt;
     } else {
         nxt.t = cur.t;
         nxt.steps = cur.steps;
@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
             cur.state = d.next_state;
             break;
         }
-        if (rank == 0 && t == 0 && C.fixed_dt <= 0 && C.dt_log && cur.steps < C.dt_cap)
+        if (rank == 0 && t == 0 && !C.fixed_mode && C.dt_log && cur.steps < C.dt_cap)
             C.dt_log[cur.steps] = d.dt;
         if (!face_ok) {
             errb |= kErrRiemann;
@@ -1246,6 +1246,17 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
         cfg.attrs = at;                                                                          \
         cfg.numAttrs = 1;                                                                        \
         return (int)cudaLaunchKernelExC(&cfg, f, args);                                          \
+    }                                                                                            \
+    int NAME##_step2d_ctas_per_sm(int shields) {                                                 \
+        const void* f = shields ? (const void*)silt_dev::step2d_kernel<S, true>                  \
+                                : (const void*)silt_dev::step2d_kernel<S, false>;                \
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
+                             (int)sizeof(silt_dev::StepSmem));                                   \
+        int per_sm = 0;                                                                          \
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kStepThreads,              \
+                                                          sizeof(silt_dev::StepSmem)) != cudaSuccess) \
+            per_sm = 0;                                                                          \
+        return per_sm;                                                                           \
     }                                                                                            \
     int NAME##_step1d_coop_blocks(int shields) {                                                 \
         int per_sm = 0, sms = 0, dev = 0;                                                        \

@@ -43,7 +43,7 @@ struct Slot {
 struct Control {
     Slot slot[3];
     double t_end;
-    double fixed_dt;      // > 0: step_1d/step_2d with a caller dt
+    double fixed_dt;      // the caller's dt when fixed_mode is set
     long long max_steps;
     long long dt_cap;
     double* dt_log;
@@ -52,7 +52,8 @@ struct Control {
     unsigned int err_claim;
     unsigned int err_bits;
     int err_col, err_row;
-    int pad_;
+    int fixed_mode;       // 1: step_1d/step_2d with the caller's dt, applied as
+                          // given (0, negative or NaN included), like the reference
     double err_info[6];
 };
 

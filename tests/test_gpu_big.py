@@ -1,0 +1,191 @@
+"""GPU parity at BASELINE's own sizes, pinned to the REFERENCE itself.
+
+The fixtures (tests/golden/golden_big.{json,npz}, made by
+tests/golden/make_golden_big.py from oracle/_ref — the unmodified reference
+core) hold a 64-bit digest of every row of every field of the reference's
+final state, its full dt log and t_final:
+
+  C3   1024^2 dune, 1000 steps (BASELINE configs[2]), whole grid
+  C4w  the 16384^2 dune (configs[3]), 500 steps, on the window around the mound
+       that is bit-for-bit the full grid's (the rest stays exactly uniform)
+  C5   the random bed (configs[4]) per-GPU tile 8192 x 4096, 100 steps
+
+STRICT (the reference's arithmetic) must match every row digest — i.e. every
+cell bit for bit — and the dt log exactly.  FAST (the production kernels) is
+held to the north-star bar against STRICT on the FULL field: per field
+||a - b||_inf / ||b||_inf <= 1e-9 (h, hu, hv and zb each on its own scale),
+dt log within 1e-12 relative, identical step count.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR, normwise
+from paper_1307_0491_b200 import abi, scenarios
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-9
+DT_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def big():
+    data = np.load(os.path.join(GOLDEN_DIR, "golden_big.npz"))
+    with open(os.path.join(GOLDEN_DIR, "golden_big.json")) as fh:
+        meta = json.load(fh)
+    return data, meta
+
+
+@pytest.fixture(scope="module")
+def N():
+    from paper_1307_0491_b200 import native
+    native.lib()
+    return native
+
+
+def row_digests(field: np.ndarray) -> np.ndarray:
+    """Same digest as make_golden_big.row_digests (BLAKE2b-64 per row/field)."""
+    ny = field.shape[0]
+    out = np.empty((ny, 4), dtype=np.uint64)
+    for f in range(4):
+        plane = np.ascontiguousarray(field[:, :, f])
+        for j in range(ny):
+            out[j, f] = np.frombuffer(hashlib.blake2b(plane[j].tobytes(), digest_size=8).digest(),
+                                      dtype="<u8")[0]
+    return out
+
+
+def assert_rows_match(got: np.ndarray, want: np.ndarray, what: str):
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, (f"{what}: {len(bad)} (row, field) digests differ, first "
+                           f"{bad[:5].tolist()}")
+
+
+def _run_host(N, p, init, steps, variant):
+    s = N.Solver(p, variant=variant)
+    s.upload(init)
+    s.begin(max_steps=steps, dt_cap=steps)
+    st = s.run(batch=100)
+    out = s.download()
+    log = s.dt_log(st.steps)
+    s.close()
+    return out, st, log
+
+
+def _check_fast(fo, so, flog, slog, label):
+    err = normwise(fo, so)
+    dterr = float(np.max(np.abs(flog - slog) / slog))
+    print(f"{label}: FAST vs STRICT per-field normwise h, hu, hv, zb = {err.tolist()}, "
+          f"dt {dterr:.2e}")
+    assert dterr <= DT_TOL
+    assert np.all(err <= FIELD_TOL), err
+
+
+def test_c3_full_field_vs_reference(N, big):
+    """C3 1024^2 x 1000 steps: STRICT equals the reference on every cell (row
+    digests), dt log and t_final bitwise; FAST within the bar on every field."""
+    data, meta = big
+    m = meta["cases"]["C3"]
+    p, init, steps = scenarios.dune_2d(1024, steps=1000)
+    assert_rows_match(row_digests(init), data["C3_init_rows"], "C3 initial field")
+    so, sst, slog = _run_host(N, p, init, steps, abi.VARIANT_STRICT)
+    assert sst.steps == m["steps"] == steps
+    assert sst.t == m["t_final"]
+    assert np.array_equal(slog, data["C3_dt"])
+    assert_rows_match(row_digests(so), data["C3_rows"], "C3 STRICT vs reference")
+    fo, fst, flog = _run_host(N, p, init, steps, abi.VARIANT_FAST)
+    assert fst.steps == steps
+    _check_fast(fo, so, flog, slog, "C3 1000 steps")
+
+
+def test_c5_tile_vs_reference(N, big):
+    """C5 random bed, the 8192 x 4096 per-GPU tile x 100 steps (every face on
+    the full fluid-outer solver): STRICT equals the reference on every cell and
+    on the dt log; FAST within the bar on every field."""
+    data, meta = big
+    m = meta["cases"]["C5"]
+    p, init, _ = scenarios.random_bed_2d(8192, 4096)
+    steps = m["steps"]
+    assert_rows_match(row_digests(init), data["C5_init_rows"],
+                      "C5 initial field (host generator differs from the fixture's)")
+    so, sst, slog = _run_host(N, p, init, steps, abi.VARIANT_STRICT)
+    assert sst.steps == steps and sst.t == m["t_final"]
+    assert np.array_equal(slog, data["C5_dt"])
+    assert_rows_match(row_digests(so), data["C5_rows"], "C5 STRICT vs reference")
+    fo, fst, flog = _run_host(N, p, init, steps, abi.VARIANT_FAST)
+    assert fst.steps == steps
+    _check_fast(fo, so, flog, slog, "C5 tile 100 steps")
+
+
+def _c4_device_init(torch, n, device):
+    """C4 initial field built on the device, bitwise equal to
+    scenarios.dune_2d(n) (one IEEE multiply and one add per cell)."""
+    dx = 1000.0 / n
+    wx = torch.from_numpy(scenarios._sine_bump(scenarios._centres(n, dx), 300.0, 200.0)).to(device)
+    wy = torch.from_numpy(scenarios._sine_bump(scenarios._centres(n, dx), 400.0, 200.0)).to(device)
+    init = torch.zeros((n, n, 4), dtype=torch.float64, device=device)
+    zb = 0.1 + torch.outer(wy, wx)
+    init[..., 0] = 10.0 - zb
+    init[..., 1] = 10.0
+    init[..., 3] = zb
+    return init
+
+
+def test_c4_full_grid_vs_reference(N, big):
+    """C4 (16384^2, 500 steps — BASELINE configs[3] exactly) on the full grid.
+    STRICT: the window around the mound equals the reference's window run on
+    every cell (row digests; see make_golden_big.py for why the window is
+    exact), every cell outside it is still the uniform far-field state, and
+    the dt log and t_final are bitwise the reference's.  FAST: within the bar
+    against STRICT on all 2.7e8 cells, per field."""
+    import torch
+    data, meta = big
+    m = meta["cases"]["C4w"]
+    (x0, x1), (y0, y1) = m["window"]["x"], m["window"]["y"]
+    n = m["window"]["n"]
+    steps = m["steps"]
+    dev = torch.device("cuda")
+    p, _, _ = scenarios.dune_2d(64)
+    p = abi.make_problem(2, n, n, 1000.0 / n, 1000.0 / n, a_g=p.a_g, cfl=p.cfl)
+    init = _c4_device_init(torch, n, dev)
+    win0 = init[y0:y1, x0:x1].cpu().numpy()
+    assert_rows_match(row_digests(win0), data["C4w_init_rows"], "C4 initial window")
+    del win0
+    far = torch.tensor([9.9, 10.0, 0.0, 0.1], dtype=torch.float64, device=dev)
+    outs, logs = {}, {}
+    for name, variant in (("strict", abi.VARIANT_STRICT), ("fast", abi.VARIANT_FAST)):
+        s = N.Solver(p, variant=variant)
+        torch.cuda.synchronize()
+        s.upload_device(init.data_ptr())
+        s.begin(max_steps=steps, dt_cap=steps)
+        st = s.run(batch=100)
+        assert st.steps == steps
+        if name == "strict":
+            assert st.t == m["t_final"]
+        out = torch.empty_like(init)
+        s.download_device(out.data_ptr())
+        logs[name] = s.dt_log(steps)
+        s.close()
+        outs[name] = out
+        torch.cuda.synchronize()
+    del init
+    so, fo = outs["strict"], outs["fast"]
+    assert np.array_equal(logs["strict"], data["C4w_dt"])
+    assert_rows_match(row_digests(so[y0:y1, x0:x1].cpu().numpy()), data["C4w_rows"],
+                      "C4 STRICT window vs reference")
+    outside = torch.ones((n, n), dtype=torch.bool, device=dev)
+    outside[y0:y1, x0:x1] = False
+    assert bool((so[outside] == far).all()), "STRICT: far field outside the window changed"
+    err = np.array([float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max())
+                    for f in range(4)])
+    dterr = float(np.max(np.abs(logs["fast"] - logs["strict"]) / logs["strict"]))
+    print(f"C4 500 steps: FAST vs STRICT per-field normwise h, hu, hv, zb = {err.tolist()}, "
+          f"dt {dterr:.2e}")
+    assert dterr <= DT_TOL
+    assert np.all(err <= FIELD_TOL), err

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import kats
-from conftest import momentum_normwise, normwise, problem_from_meta
+from conftest import normwise, problem_from_meta
 from paper_1307_0491_b200 import abi, scenarios
 
 pytestmark = pytest.mark.gpu
@@ -151,6 +151,36 @@ def test_step_padded_matches_restatement(N, restatement):
     assert np.array_equal(got, ref)
     got = N.step_padded(p, pd, dt, abi.VARIANT_FAST)
     assert np.all(normwise(got[1:-1, 1:-1], ref[1:-1, 1:-1]) <= 1e-12)
+
+
+@pytest.mark.parametrize("variant", ["strict", "fast"])
+def test_step_padded_caller_dt_as_given(N, restatement, variant):
+    """step_1d/step_2d apply the caller's dt as given (src/stepper.cpp:118-189):
+    dt = 0 leaves the field unchanged (also on an all-dry field, where cfl_dt
+    would throw), dt < 0 steps backwards like the reference, and a NaN dt
+    fails check_depth with the reference's runtime_error message."""
+    rng = np.random.default_rng(11)
+    ny, nx = 6, 33
+    p = abi.make_problem(2, nx, ny, 0.7, 0.9, a_g=0.4)
+    pd = np.zeros((ny + 2, nx + 2, 4))
+    pd[..., 0] = rng.uniform(0.5, 2.0, pd.shape[:2])
+    pd[..., 1] = pd[..., 0] * rng.uniform(-1, 1, pd.shape[:2])
+    pd[..., 3] = rng.uniform(-0.2, 0.2, pd.shape[:2])
+    v = VARIANTS[variant]
+    got = N.step_padded(p, pd, 0.0, v)
+    assert np.array_equal(got, restatement.step_padded(p, pd, 0.0))
+    assert np.array_equal(got[1:-1, 1:-1], pd[1:-1, 1:-1])
+    dt = -0.2 * restatement.cfl_dt(p, pd[1:-1, 1:-1])
+    ref = restatement.step_padded(p, pd, dt)
+    got = N.step_padded(p, pd, dt, v)
+    if variant == "strict":
+        assert np.array_equal(got, ref)
+    else:
+        assert np.all(normwise(got[1:-1, 1:-1], ref[1:-1, 1:-1]) <= 1e-12)
+    dry = np.zeros_like(pd)
+    assert np.array_equal(N.step_padded(p, dry, 0.0, v), dry)
+    with pytest.raises(N.SiltRuntimeError, match="negative depth"):
+        N.step_padded(p, pd, float("nan"), v)
 
 
 def test_snapshots_pause_and_land(N, golden):
@@ -308,10 +338,8 @@ def test_c4_full_size_properties(N):
     assert sst.steps == steps
     assert np.max(np.abs(flog - slog) / slog) <= DT_TOL
     err = normwise(fo, so)
-    print("C4 fast vs strict, per-field normwise:", err,
-          "hv vs momentum scale:", momentum_normwise(fo, so))
-    assert np.all(err[[0, 1, 3]] <= FIELD_TOL), err
-    assert momentum_normwise(fo, so) <= FIELD_TOL
+    print("C4 40 steps fast vs strict, per-field normwise h, hu, hv, zb:", err.tolist())
+    assert np.all(err <= FIELD_TOL), err
 
 
 @pytest.mark.slow
@@ -320,7 +348,7 @@ def test_c4_1000_steps_fast_vs_strict(N):
     FAST (the production kernels: quiescent skip, launch order, FMA,
     reciprocals) against STRICT (the reference's arithmetic, bitwise with the
     reference on every smaller fixture): identical step count, dt sequence
-    within 1e-12, fields within 1e-9 normwise (hv against the momentum scale).
+    within 1e-12, fields within 1e-9 normwise (every field on its own scale).
     Fields stay on the device (built there, compared there)."""
     import torch
 
@@ -344,11 +372,9 @@ def test_c4_1000_steps_fast_vs_strict(N):
     del init
     fo, so = outs
     assert np.max(np.abs(logs[0] - logs[1]) / logs[1]) <= DT_TOL
-    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in (0, 1, 3)]
-    mom = float((fo[..., 2] - so[..., 2]).abs().max() /
-                torch.maximum(so[..., 1].abs().max(), so[..., 2].abs().max()))
-    print("C4 1000 steps fast vs strict: h, hu, zb", err, "hv/momentum", mom)
-    assert max(err) <= FIELD_TOL and mom <= FIELD_TOL
+    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in range(4)]
+    print("C4 1000 steps fast vs strict per field: h, hu, hv, zb", err)
+    assert max(err) <= FIELD_TOL
 
 
 @pytest.mark.slow
@@ -356,7 +382,7 @@ def test_c5_1000_steps_fast_vs_strict(N):
     """The north-star bar where every face takes the full solver: the C5
     random bed (8192 x 4096 per GPU, nothing quiescent) for 1000 steps, FAST
     against STRICT on the device: identical step count, dt within 1e-12,
-    fields within 1e-9 normwise (hv against the momentum scale)."""
+    fields within 1e-9 normwise (every field on its own scale)."""
     import torch
 
     import bench
@@ -378,18 +404,16 @@ def test_c5_1000_steps_fast_vs_strict(N):
         outs.append(out)
     fo, so = outs
     assert np.max(np.abs(logs[0] - logs[1]) / logs[1]) <= DT_TOL
-    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in (0, 1, 3)]
-    mom = float((fo[..., 2] - so[..., 2]).abs().max() /
-                torch.maximum(so[..., 1].abs().max(), so[..., 2].abs().max()))
-    print("C5 1000 steps fast vs strict: h, hu, zb", err, "hv/momentum", mom)
-    assert max(err) <= FIELD_TOL and mom <= FIELD_TOL
+    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in range(4)]
+    print("C5 1000 steps fast vs strict per field: h, hu, hv, zb", err)
+    assert max(err) <= FIELD_TOL
 
 
 def test_c5_full_size_fast_vs_strict(N):
     """BASELINE config 5 at its stated size and length on one GPU: the
     32768 x 8192 random bed (the 8-GPU stress test's whole grid), 300 steps,
     FAST against STRICT: identical step count, dt within 1e-12, fields within
-    1e-9 normwise (hv against the momentum scale)."""
+    1e-9 normwise (every field on its own scale)."""
     import torch
 
     import bench
@@ -413,11 +437,9 @@ def test_c5_full_size_fast_vs_strict(N):
         torch.cuda.synchronize()
     fo, so = outs
     assert np.max(np.abs(logs[0] - logs[1]) / logs[1]) <= DT_TOL
-    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in (0, 1, 3)]
-    mom = float((fo[..., 2] - so[..., 2]).abs().max() /
-                torch.maximum(so[..., 1].abs().max(), so[..., 2].abs().max()))
-    print("C5 full size 300 steps fast vs strict: h, hu, zb", err, "hv/momentum", mom)
-    assert max(err) <= FIELD_TOL and mom <= FIELD_TOL
+    err = [float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max()) for f in range(4)]
+    print("C5 full size 300 steps fast vs strict per field: h, hu, hv, zb", err)
+    assert max(err) <= FIELD_TOL
 
 
 @pytest.mark.slow

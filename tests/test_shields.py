@@ -22,7 +22,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import momentum_normwise, normwise, problem_from_meta
+from conftest import normwise, problem_from_meta
 from paper_1307_0491_b200 import abi
 
 FORMULAS = list(abi.SHIELDS_FORMULAS)
@@ -269,8 +269,8 @@ def test_gpu_runs(N, golden_shields, variant):
         assert abs(t - m["t_final"]) <= 1e-12 * m["t_final"], case
         assert np.max(np.abs(log - ref_log) / ref_log) <= 1e-12, case
         err = normwise(out, ref)
-        assert np.all(err[[0, 1, 3]] <= tol), (case, err)
-        assert momentum_normwise(out, ref) <= tol, case
+        print(f"{case} {variant}: per-field normwise h, hu, hv, zb = {err.tolist()}")
+        assert np.all(err <= tol), (case, err)
         if case.startswith("frozen"):
             assert np.array_equal(out[..., 3], data[f"{case}_init"][..., 3])
 
