@@ -341,6 +341,14 @@ int error_from(const Control& c, unsigned bits) {
     }
     if (bits & silt_dev::kErrNegDepth) return fail(SILT_ERR_RUNTIME, kNegDepthMsg);
     if (bits & silt_dev::kErrDry) return fail(SILT_ERR_INVALID, "cfl_dt: field is entirely dry");
+    if (bits & silt_dev::kErrPeer) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf,
+                      "p2p: rank %d did not publish step %d within the peer timeout "
+                      "(SILT_P2P_TIMEOUT_MS); the peer process died or hung",
+                      c.err_col, c.err_row);
+        return fail(SILT_ERR_RUNTIME, buf);
+    }
 
     return fail(SILT_ERR_RUNTIME, "step: device error");
 }
@@ -350,6 +358,22 @@ int error_from(const Control& c, unsigned bits) {
 extern "C" {
 
 int silt_abi_version(void) { return SILT_ABI_VERSION; }
+
+// Diagnostics (not part of the drop-in API): bounds-check counters of a
+// -DSILT_CHECKED build, summed over both variants' kernels, then reset.
+// out[4] = {violations, first code, first a, first b}; returns 1 in a checked
+// build, 0 otherwise (counters then stay 0).
+int silt_debug_checks(unsigned long long* out) {
+    unsigned long long a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
+    const int ca = silt_fast_debug_checks(a);
+    const int cb = silt_strict_debug_checks(b);
+    if (out) {
+        out[0] = a[0] + b[0];
+        const unsigned long long* first = a[0] ? a : b;
+        for (int k = 1; k < 4; ++k) out[k] = first[k];
+    }
+    return ca | cb;
+}
 
 int silt_abi_sizes(int64_t* sizes, int n) {
     const int64_t all[6] = {sizeof(silt_bc),       sizeof(silt_problem), sizeof(silt_strip),
@@ -1065,10 +1089,16 @@ __global__ void push_release_kernel(const Control* local, int slot, Control* con
 }
 
 // p2p: acquire (system scope) every peer's flag before the step that reads
-// their rows and maxima; the stream has already waited for the values, so
-// the loop normally exits at once
+// their rows and maxima.  The wait is bounded: a peer that has not published
+// step `expect` within timeout_ns (dead or hung rank) raises kErrPeer in the
+// slot the next launch reads, so that launch and every later one stop
+// (decide: FAILED) and the host reports which rank missed which step, instead
+// of the GPU spinning forever.
 __global__ void acquire_flags_kernel(const unsigned* flags, int world, int rank,
-                                     unsigned expect) {
+                                     unsigned expect, Control* ctl, int slot,
+                                     unsigned long long timeout_ns) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (int j = threadIdx.x; j < world; j += blockDim.x) {
         if (j == rank) continue;
         unsigned v;
@@ -1076,7 +1106,18 @@ __global__ void acquire_flags_kernel(const unsigned* flags, int world, int rank,
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + j)
                          : "memory");
             if ((int)(v - expect) >= 0) break;
-            __nanosleep(1000);
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) {
+                atomicOr(&ctl->slot[slot].err, silt_dev::kErrPeer);
+                if (atomicCAS(&ctl->err_claim, 0u, 1u) == 0u) {
+                    ctl->err_bits = silt_dev::kErrPeer;
+                    ctl->err_col = j;            // the rank that missed the step
+                    ctl->err_row = (int)expect;  // the step it did not publish
+                }
+                break;
+            }
+            __nanosleep(500);
         }
     }
 }
@@ -1910,28 +1951,14 @@ extern "C" int silt_solver_capture_write(silt_solver* s, double time, const char
 // ---- multi-process strips over peer memory ----------------------------------------
 namespace {
 
-using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-int stream_mem_ops(WaitValueFn* wait, WriteValueFn* write) {
-    static WaitValueFn w = nullptr;
-    static WriteValueFn r = nullptr;
-    if (!w || !r) {
-        cudaDriverEntryPointQueryResult q;
-        void* f = nullptr;
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) !=
-                cudaSuccess || !f)
-            return fail(SILT_ERR_UNSUPPORTED, "p2p: cuStreamWaitValue32 unavailable");
-        w = reinterpret_cast<WaitValueFn>(f);
-        f = nullptr;
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) !=
-                cudaSuccess || !f)
-            return fail(SILT_ERR_UNSUPPORTED, "p2p: cuStreamWriteValue32 unavailable");
-        r = reinterpret_cast<WriteValueFn>(f);
-    }
-    *wait = w;
-    *write = r;
-    return SILT_OK;
+// Bound of the per-step wait for the peers (SILT_P2P_TIMEOUT_MS, default 60 s).
+unsigned long long p2p_timeout_ns() {
+    static const unsigned long long ns = [] {
+        const char* e = std::getenv("SILT_P2P_TIMEOUT_MS");
+        const long long ms = e ? std::atoll(e) : 60000;
+        return (unsigned long long)(ms > 0 ? ms : 60000) * 1000000ull;
+    }();
+    return ns;
 }
 
 }  // namespace
@@ -1964,9 +1991,6 @@ extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
     if (!s->p2p_flags) return fail(SILT_ERR_INVALID, "p2p: export before connect");
     if ((south >= 0) != (bool)s->strip.south_neighbor || (north >= 0) != (bool)s->strip.north_neighbor)
         return fail(SILT_ERR_INVALID, "p2p: neighbours do not match the strip");
-    WaitValueFn w;
-    WriteValueFn r;
-    if (int rc = stream_mem_ops(&w, &r)) return rc;
     CUDA_TRY(cudaSetDevice(s->device));
     std::vector<void*> rows(world, nullptr), ctls(world, nullptr), flags(world, nullptr);
     for (int j = 0; j < world; ++j) {
@@ -2006,19 +2030,15 @@ extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
     CUDA_TRY(cudaMalloc(&s->p2p_peer_flag_dev, s->p2p_peer_flag.size() * sizeof(unsigned*)));
     CUDA_TRY(cudaMemcpy(s->p2p_peer_flag_dev, s->p2p_peer_flag.data(),
                         s->p2p_peer_flag.size() * sizeof(unsigned*), cudaMemcpyHostToDevice));
-    // probe the mechanism once (remote atomics, remote flag writes, local
-    // waits) so that a driver can fall back before its first step
+    // probe the mechanism once (remote atomics, remote flag writes, the
+    // acquire) so that a driver can fall back before its first step
     {
-        const CUstream cs = reinterpret_cast<CUstream>(s->stream);
         push_release_kernel<<<1, 32, 0, s->stream>>>(s->ctl, 0, s->p2p_peer_ctl,
                                                      s->p2p_peer_flag_dev, world - 1,
                                                      s->p2p_count);
         CUDA_TRY(cudaGetLastError());
-        (void)r;
-        if (w(cs, reinterpret_cast<CUdeviceptr>(s->p2p_flags), 0, CU_STREAM_WAIT_VALUE_GEQ) !=
-            CUDA_SUCCESS)
-            return fail(SILT_ERR_UNSUPPORTED, "p2p: stream waits unsupported");
-        acquire_flags_kernel<<<1, 32, 0, s->stream>>>(s->p2p_flags, world, rank, 0u);
+        acquire_flags_kernel<<<1, 32, 0, s->stream>>>(s->p2p_flags, world, rank, 0u, s->ctl, 0,
+                                                      p2p_timeout_ns());
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(s->stream));
     }
@@ -2034,26 +2054,17 @@ extern "C" int silt_solver_p2p_step(silt_solver* s, int n) {
     if (!s->begun || !s->begun_after_connect)
         return fail(SILT_ERR_INVALID, "silt_solver_p2p_step: call silt_solver_begin after connect");
     if (int rc = check_cfl(s->prob.cfl)) return rc;
-    WaitValueFn wait;
-    WriteValueFn write;
-    if (int rc = stream_mem_ops(&wait, &write)) return rc;
     CUDA_TRY(cudaSetDevice(s->device));
-    const CUstream cs = reinterpret_cast<CUstream>(s->stream);
-    (void)write;
+    const unsigned long long timeout = p2p_timeout_ns();
     for (int k = 0; k < n; ++k) {
         const unsigned c = ++s->p2p_count;
         if (c > 1) {
-            // every rank finished step c-1 (its rows and maxima are here): the
-            // stream waits without occupying the GPU, then one thread acquires
-            // the flags at system scope so the step observes the peers' writes
-            for (int j = 0; j < s->p2p_world; ++j) {
-                if (j == s->p2p_rank) continue;
-                if (wait(cs, reinterpret_cast<CUdeviceptr>(s->p2p_flags + j), c - 1,
-                         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                    return fail(SILT_ERR_CUDA, "p2p: cuStreamWaitValue32 failed");
-            }
+            // every rank finished step c-1 (its rows and maxima are here): one
+            // warp acquires the peers' flags at system scope, with a bounded
+            // wait, so the step observes the peers' writes
             acquire_flags_kernel<<<1, 32, 0, s->stream>>>(s->p2p_flags, s->p2p_world, s->p2p_rank,
-                                                          c - 1);
+                                                          c - 1, s->ctl, (int)(s->launches % 3),
+                                                          timeout);
             ++s->kernel_count;
         }
         launch_step(s);

@@ -183,6 +183,7 @@ __device__ __forceinline__ void ghost_transform(const StepArgs& A, int side, dou
 
 __device__ __forceinline__ void load_interior(const StepArgs& A, int p, int col, int row,
                                               double c[4]) {
+    if (SILT_VIOLATED(row >= 0 && row < A.ny && col >= 0 && col < A.nx, 1, row, col)) return;
     const size_t off = (size_t)row * A.pitch + col;
 #pragma unroll
     for (int f = 0; f < 4; ++f) c[f] = __ldg(A.state[p][f] + off);
@@ -235,6 +236,7 @@ __device__ __forceinline__ void load_cell(const StepArgs& A, int p, int col, int
 // for a neighbour strip.
 __device__ __forceinline__ void write_edges(const StepArgs& A, int q, int col, int row,
                                             const double c[4]) {
+    if (SILT_VIOLATED(col >= 0 && col < A.nx, 2, row, col)) return;
     if (row == 0) {
         if (A.south_nbr) {
 #pragma unroll
@@ -413,6 +415,9 @@ __device__ __forceinline__ void cp_async8_s(unsigned dst, const double* src) {
 __device__ __forceinline__ void prefetch_row(const StepArgs& A, const RowSrc& s, int p, int row,
                                              unsigned dst) {
     constexpr unsigned kFieldBytes = kStepThreads * sizeof(double);
+    if (SILT_VIOLATED(row >= -1 && row <= A.ny && s.col_clamped >= 0 && s.col_clamped < A.nx,
+                      3, row, s.col_clamped))
+        return;
     if (row >= 0 && row < A.ny) {
         const size_t off = (size_t)row * s.stride;
 #pragma unroll
@@ -625,6 +630,9 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             have = false;
         }
         buf = buf == SILT_RING - 1 ? 0 : buf + 1;
+        if (SILT_VIOLATED(blockDim.x == kStepThreads && buf >= 0 && buf < SILT_RING, 4, buf,
+                          blockDim.x))
+            return;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
 
@@ -656,7 +664,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                 quiet_prev = quiet;
                 if (!skip) qvalid = false;
                 if (skip) {
-                    if (owned) {  // row r-1 is unchanged: o == c
+                    if (owned && !SILT_VIOLATED(r - 1 >= 0 && r - 1 < A.ny && col < A.nx, 6,
+                                                r - 1, col)) {  // row r-1 is unchanged: o == c
                         const size_t off = (size_t)(r - 1) * A.pitch;
                         out0[off] = c[0];
                         out0[off + plane] = c[1];
@@ -695,7 +704,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                                 break;
                             }
                             buf = buf == SILT_RING - 1 ? 0 : buf + 1;
-                            if (owned) {  // row r is unchanged: o == c
+                            if (owned && !SILT_VIOLATED(r >= 0 && r < A.ny && col < A.nx, 7, r,
+                                                        col)) {  // row r is unchanged: o == c
                                 const size_t off = (size_t)r * A.pitch;
                                 out0[off] = c[0];
                                 out0[off + plane] = c[1];
@@ -736,6 +746,8 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             o[1] = sh_xs[1][t] - cy * (fy.hv - sh_fy[2][t]);
             o[3] = sh_xs[3][t] - cy * (fy.z - sh_fy[3][t]);
             if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
+            if (SILT_VIOLATED(r - 1 >= 0 && r - 1 < A.ny && col >= 0 && col < A.nx, 5, r - 1, col))
+                continue;
             const size_t off = (size_t)(r - 1) * A.pitch;
             out0[off] = o[0];
             out0[off + plane] = o[1];
@@ -835,8 +847,9 @@ __device__ __forceinline__ void step1d_body(const StepArgs& A, int li) {
         o[2] = c[2] - c1 * (fx.hv - lhv);
         o[3] = c[3] - c1 * (fx.z - lz);
         if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, 0, nullptr, nxt);
+        if (!SILT_VIOLATED(col >= 0 && col < A.nx, 8, 0, col))
 #pragma unroll
-        for (int f = 0; f < 4; ++f) A.state[q][f][col] = o[f];
+            for (int f = 0; f < 4; ++f) A.state[q][f][col] = o[f];
         double ssx, ssy;
         cell_speeds<S, SH>(A, o, ssx, ssy);
         reduce_fold(A, R, o, ssx, ssy);
@@ -926,8 +939,12 @@ __global__ void __launch_bounds__(kCluster1dThreads, 1)
     const bool ghost = col == -1 || col == nx;
     const int bct = ghost ? A.bc_type[side] : SILT_BC_OUTFLOW;
     if (ghost) src = (bct == SILT_BC_PERIODIC) ? (col < 0 ? nx - 1 : 0) : (col < 0 ? 0 : nx - 1);
-    const int owner = src / kCluster1dCells, idx = src - owner * kCluster1dCells;
-    const int oi = owned ? col - base : 0;  // this lane's slot in the CTA's line
+    int owner = src / kCluster1dCells, idx = src - owner * kCluster1dCells;
+    int oi = owned ? col - base : 0;  // this lane's slot in the CTA's line
+    if (SILT_VIOLATED(oi >= 0 && oi < kCluster1dCells && idx >= 0 && idx < kCluster1dCells &&
+                          owner >= 0 && owner < (int)cl.num_blocks(),
+                      9, oi, owner))
+        oi = idx = owner = 0;  // checked build: counted, clamped (no early exit: barriers)
     double* const own_cell[2] = {&s_line[0][0][oi], &s_line[1][0][oi]};
     double* const src_cell[2] = {cl.map_shared_rank(&s_line[0][0][idx], owner),
                                  cl.map_shared_rank(&s_line[1][0][idx], owner)};
@@ -1183,6 +1200,19 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
 
 }  // namespace silt_dev
 
+#ifdef SILT_CHECKED
+#define SILT_DEBUG_CHECKS_BODY                                                                 \
+    cudaDeviceSynchronize();                                                                   \
+    cudaMemcpyFromSymbol(out, silt_dev::g_check, sizeof(unsigned long long) * 4);              \
+    const unsigned long long z[4] = {0, 0, 0, 0};                                              \
+    cudaMemcpyToSymbol(silt_dev::g_check, z, sizeof z);                                        \
+    return 1;
+#else
+#define SILT_DEBUG_CHECKS_BODY \
+    (void)out;                 \
+    return 0;
+#endif
+
 // Explicit instantiation hooks, defined by each TU with its own S; the law
 // kind (A.P.shields) picks the kernel instantiation at launch.
 #define SILT_DEFINE_LAUNCHERS(S, NAME)                                                          \
@@ -1246,6 +1276,9 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
         cfg.attrs = at;                                                                          \
         cfg.numAttrs = 1;                                                                        \
         return (int)cudaLaunchKernelExC(&cfg, f, args);                                          \
+    }                                                                                            \
+    int NAME##_debug_checks(unsigned long long* out) {                                           \
+        SILT_DEBUG_CHECKS_BODY                                                                   \
     }                                                                                            \
     int NAME##_step2d_ctas_per_sm(int shields) {                                                 \
         const void* f = shields ? (const void*)silt_dev::step2d_kernel<S, true>                  \

@@ -9,6 +9,7 @@
     int NAME##_step1d_coop(const StepArgs& A, int li0, int n, dim3 grid, cudaStream_t st);   \
     int NAME##_step1d_coop_blocks(int shields);                                              \
     int NAME##_step2d_ctas_per_sm(int shields);                                              \
+    int NAME##_debug_checks(unsigned long long* out);                                        \
     int NAME##_step1d_cluster(const StepArgs& A, int li0, int n, int ctas, cudaStream_t st); \
     void NAME##_reduce(const StepArgs& A, int li, int blocks, cudaStream_t st);              \
     void NAME##_faces(const silt_dev::Params& P, const double* L, const double* R,           \

@@ -22,6 +22,27 @@ namespace silt_dev {
 #ifdef SILT_STATS
 __device__ unsigned long long g_stats[8];
 #endif
+// ---- checked build (-DSILT_CHECKED) ------------------------------------------
+// compute-sanitizer is closed on this GPU pool, so the kernels carry their own
+// bounds checks in a diagnostics build: every global row/column index and
+// every ring slot is validated before the access; a violation is counted
+// (first offender recorded) and the access skipped, so the checked build
+// never faults.  tools/sanitize_cases.py runs every device path with it and
+// reads the counters (silt_debug_checks).  Compiled out otherwise.
+#ifdef SILT_CHECKED
+static __device__ unsigned long long g_check[4];  // violations, first code, first a, first b
+static __device__ __noinline__ bool check_fail(int code, long long a, long long b) {
+    if (atomicAdd(&g_check[0], 1ull) == 0ull) {
+        g_check[1] = (unsigned long long)code;
+        g_check[2] = (unsigned long long)a;
+        g_check[3] = (unsigned long long)b;
+    }
+    return true;
+}
+#define SILT_VIOLATED(ok, code, a, b) (!(ok) && silt_dev::check_fail((code), (a), (b)))
+#else
+#define SILT_VIOLATED(ok, code, a, b) false
+#endif
 #ifdef SILT_TRACE
 // diagnostics build only: per-CTA records of the FAST 2D step kernel
 // {start ns, end ns, smid | blockIdx.x << 16, row block | full rows << 16}

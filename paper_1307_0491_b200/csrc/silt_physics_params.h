@@ -7,6 +7,9 @@ namespace silt_dev {
 constexpr unsigned kErrNegDepth = 1u;  // check_depth (src/stepper.cpp:91-100)
 constexpr unsigned kErrRiemann = 2u;   // interface_riemann (src/riemann.cpp:332-337)
 constexpr unsigned kErrDry = 4u;       // cfl_dt all dry (src/stepper.cpp:56)
+constexpr unsigned kErrPeer = 8u;      // multi-process strips: a peer rank missed a step
+                                       // (no reference analogue: run_parallel's workers
+                                       // share one process; a dead worker rethrows)
 
 // Physics (include/silt/physics.hpp:7-11) + bedload law (bedload.hpp:32-52) +
 // the interface safety factor (Scenario::safety, scenarios.hpp:47).

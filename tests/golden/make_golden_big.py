@@ -31,6 +31,15 @@ Cases
   C5   BASELINE configs[4]'s generator (scenarios.random_bed_2d) on the per-GPU
        tile 8192 x 4096 (bench.py --workload C5 at N = 1), A_g = 0.01, CFL 0.4,
        100 steps: every face takes the full solver.
+  C4w40_fma / C3_fma
+       The reference's own rounding spread: the same reference sources compiled
+       with FMA contraction (oracle/_ref/libsilt_ref_fma.so, `make -C oracle
+       ref_fma`) against the default build, per field (normwise), on the C4
+       window after 40 steps and on C3 after 1000 steps.  Early in the C4 run hv
+       is O(1e-7) while the y-momentum fluxes it is the difference of are
+       O(500), so its per-field ratio there measures rounding: the reference
+       disagrees with itself by ~1e-5 (tests/test_gpu_parity.py uses this as
+       the hv bar of its 40-step C4 property test).
 """
 from __future__ import annotations
 
@@ -99,8 +108,33 @@ def c4_window_problem(margin: int = C4_MARGIN):
     return p, init, ((x0, x1), (y0, y1))
 
 
+def fma_spread(name: str, threads: int):
+    """Per-field normwise difference between the FMA-contracted reference
+    build and the default build (both the unmodified reference sources)."""
+    import oracle as O
+    R = O.reference()
+    F = O.CpuSolver(os.path.join(ROOT, "oracle", "_ref", "libsilt_ref_fma.so"), "ref")
+    if name == "C4w40_fma":
+        p, init, win = c4_window_problem(48)
+        steps, py = 40, 64
+    else:
+        p, init, steps = S.dune_2d(1024, steps=1000)
+        py = 64
+    a = R.run_blocks(p, init, steps, py, threads)
+    b = F.run_blocks(p, init, steps, py, threads)
+    A, B = a[0].reshape(-1, 4), b[0].reshape(-1, 4)
+    meta = {"steps": steps, "nx": p.nx, "ny": p.ny,
+            "max_abs": np.abs(A).max(0).tolist(),
+            "fma_vs_ref_normwise": (np.abs(A - B).max(0) / np.abs(A).max(0)).tolist(),
+            "fma_vs_ref_dt": float(np.max(np.abs(a[3] - b[3]) / a[3]))}
+    print(name, meta, flush=True)
+    return meta, {}
+
+
 def run_case(name: str, threads: int):
     import oracle as O
+    if name.endswith("_fma"):
+        return fma_spread(name, threads)
     R = O.reference()
     meta: dict = {}
     if name == "C3":

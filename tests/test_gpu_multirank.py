@@ -89,6 +89,63 @@ def test_strip_runner_ranks_on_one_gpu(tmp_path, golden, world, case):
             assert np.all(normwise(field, data[f"{case}_final"]) <= 1e-9)
 
 
+def _hung_peer_worker(rank, world, port, case, out_dir):
+    """Rank 1 stops stepping after begin (a hung or dying peer); rank 0's
+    bounded peer wait must turn that into an error instead of spinning."""
+    import time
+    os.environ["SILT_P2P_TIMEOUT_MS"] = "2000"
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0")
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    from conftest import problem_from_meta
+    from paper_1307_0491_b200 import abi, native
+    from paper_1307_0491_b200.distributed import StripRunner, init_dist
+    m, init = case
+    p = problem_from_meta(m)
+    torch.cuda.set_device(0)
+    init_dist(world, backend="gloo")
+    runner = StripRunner(p, world, rank, device=0, variant=abi.VARIANT_FAST)
+    runner.upload_host(np.ascontiguousarray(init[runner.j0:runner.j0 + runner.nrows]))
+    runner.begin(max_steps=m["max_steps"])
+    done = os.path.join(out_dir, "result.txt")
+    if rank == 1:  # hung: never steps; keeps its memory mapped until rank 0 is done
+        t0 = time.time()
+        while not os.path.exists(done) and time.time() - t0 < 120:
+            time.sleep(0.2)
+        os._exit(0)
+    msg = "no error"
+    t0 = time.time()
+    try:
+        runner.step(4)
+        runner.status()
+    except native.SiltRuntimeError as e:
+        msg = str(e)
+    el = time.time() - t0
+    with open(done + ".tmp", "w") as fh:
+        fh.write(f"{runner._p2p}\n{el}\n{msg}\n")
+    os.replace(done + ".tmp", done)
+    os._exit(0)
+
+
+def test_hung_peer_times_out(tmp_path, golden):
+    """Peer-memory strips: a rank that stops publishing its steps makes the
+    others fail with an error naming it (bounded wait in the acquire kernel,
+    SILT_P2P_TIMEOUT_MS) instead of hanging the GPU."""
+    import torch.multiprocessing as mp
+    if os.environ.get("SILT_P2P", "1") == "0":
+        pytest.skip("peer-memory path disabled")
+    data, meta = golden
+    m = meta["cases"]["rand48x32"]
+    mp.spawn(_hung_peer_worker, args=(2, _free_port(), (m, data["rand48x32_init"]),
+                                      str(tmp_path)), nprocs=2, join=True)
+    p2p, el, msg = (tmp_path / "result.txt").read_text().splitlines()[:3]
+    assert p2p == "True"
+    assert "rank 1 did not publish step 1" in msg, msg
+    assert float(el) < 30.0
+
+
 def test_uneven_partition_on_one_gpu(tmp_path, golden):
     """A work-balanced (uneven) partition through the same device path."""
     import torch.multiprocessing as mp
@@ -118,5 +175,5 @@ def test_bench_two_ranks_on_one_gpu():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
-    assert d["config"]["parallelism"] == "row strips x2"
+    assert d["layout"]["parallelism"] == "row strips x2"
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
