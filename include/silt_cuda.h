@@ -237,6 +237,13 @@ int silt_host_alloc(int64_t bytes, void** out);
 int silt_host_free(void* p);
 /* dt of steps [0, n) from the device log (n <= capacity). */
 int silt_solver_dt_log(silt_solver* s, double* host_out, int64_t n);
+/* WorkerTiming.compute_seconds (include/silt/parallel.hpp:52-57; measured at
+ * src/parallel.cpp:324-348): device seconds of this strip's step launches
+ * since timing was last enabled (CUDA events around each launch, harvested
+ * when the stream synchronises).  Synchronises; writes the current total to
+ * *compute_seconds (may be NULL); enable = 1 / 0 switches timing on / off and
+ * resets the total, enable < 0 only reads. */
+int silt_solver_timing(silt_solver* s, int enable, double* compute_seconds);
 /* Current cfl_dt of the uploaded state (synchronises). */
 int silt_solver_cfl_dt(silt_solver* s, double* dt);
 /* Multi-rank hooks. reduce_slot: device pointer to the {max_x, max_y} axis
@@ -304,6 +311,8 @@ int silt_group_resume(silt_group* g);
 int silt_group_capture_resume(silt_group* g, double* host_aos);
 int silt_group_capture_wait(silt_group* g);
 int silt_group_dt_log(silt_group* g, double* host_out, int64_t n);
+/* silt_solver_timing over the strips: per_strip[k] (py entries, may be NULL). */
+int silt_group_timing(silt_group* g, int enable, double* per_strip);
 
 /* ---- snapshot CSV, formatted on the device -------------------------------
  * write_snapshot / snapshot_to_string (src/snapshot.cpp:50-93; io.hpp:66-73):

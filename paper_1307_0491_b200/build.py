@@ -51,9 +51,10 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
-          extra: list[str] | None = None) -> str:
+          extra: list[str] | None = None, unit_flags: dict | None = None) -> str:
     """Compile the library.  `out`/`extra` build an experimental variant
-    (e.g. a different register cap) next to the default one."""
+    (e.g. a different register cap) next to the default one; `unit_flags`
+    replaces a unit's own flags (e.g. {"silt_fast.cu": ["-fmad=false"]})."""
     lib = out or LIB
     if out is None and not force and up_to_date():
         return LIB
@@ -63,6 +64,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     objs = []
     procs = []
     for src, flags in UNITS:
+        flags = (unit_flags or {}).get(src, flags)
         obj = os.path.join(libdir, src.replace(".cu", ".o"))
         objs.append(obj)
         cmd = [NVCC] + ARCH + COMMON + flags + extra + ["-c", os.path.join(CSRC, src), "-o", obj]

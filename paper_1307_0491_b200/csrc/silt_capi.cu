@@ -197,7 +197,51 @@ struct silt_solver {
     bool begun = false;
     StepArgs args{};
     dim3 step_grid;
+    // WorkerTiming split (silt_solver_timing): device time of this strip's
+    // step launches, bracketed by events and harvested when the stream syncs
+    bool timing_on = false;
+    std::vector<cudaEvent_t> tev_free;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev_pending;
+    double compute_s = 0;
 };
+
+namespace {
+// Event bracket around this strip's step work (timing builds of run_parallel's
+// WorkerTiming.compute_seconds); no-op unless silt_solver_timing enabled it.
+cudaEvent_t timing_mark(silt_solver* s) {
+    if (!s->timing_on) return nullptr;
+    cudaEvent_t e = nullptr;
+    if (!s->tev_free.empty()) {
+        e = s->tev_free.back();
+        s->tev_free.pop_back();
+    } else if (cudaEventCreate(&e) != cudaSuccess) {
+        return nullptr;
+    }
+    cudaEventRecord(e, s->stream);
+    return e;
+}
+
+void timing_close(silt_solver* s, cudaEvent_t start) {
+    if (!start) return;
+    cudaEvent_t end = timing_mark(s);
+    if (!end) {
+        s->tev_free.push_back(start);
+        return;
+    }
+    s->tev_pending.emplace_back(start, end);
+}
+
+// After a stream synchronisation: fold the completed brackets into compute_s.
+void timing_harvest(silt_solver* s) {
+    for (auto& pr : s->tev_pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) s->compute_s += 1e-3 * ms;
+        s->tev_free.push_back(pr.first);
+        s->tev_free.push_back(pr.second);
+    }
+    s->tev_pending.clear();
+}
+}  // namespace
 
 namespace {
 
@@ -290,6 +334,12 @@ int check_cfl(double cfl) {
 // part 0: the whole step; 1: the two boundary row blocks of a split step;
 // 2: its interior row blocks (and the end of the step).
 void launch_step(silt_solver* s, int part = 0) {
+    const cudaEvent_t t0 = timing_mark(s);
+    struct Close {
+        silt_solver* s;
+        cudaEvent_t t0;
+        ~Close() { timing_close(s, t0); }
+    } close_{s, t0};
     const int li = (int)(s->launches % 3);
     StepArgs a = s->args;
     dim3 grid = s->step_grid;
@@ -319,6 +369,7 @@ int read_slot(silt_solver* s, Slot* out, Control* full) {
     CUDA_TRY(cudaSetDevice(s->device));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     CUDA_TRY(cudaGetLastError());
+    timing_harvest(s);
     if (full) {
         CUDA_TRY(cudaMemcpy(full, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost));
         *out = full->slot[s->launches % 3];
@@ -604,6 +655,8 @@ int silt_solver_destroy(silt_solver* s) {
     cudaFree(s->dt_log);
     cudaFree(s->snaps);
     if (s->host_ctl) cudaFreeHost(s->host_ctl);
+    timing_harvest(s);
+    for (cudaEvent_t e : s->tev_free) cudaEventDestroy(e);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return SILT_OK;
@@ -894,10 +947,12 @@ int silt_solver_step(silt_solver* s, int n) {
             return !(e && e[0] == '2');
         }();
         if (cluster_ok && ctas <= 16 && !s->cluster_failed) {
+            const cudaEvent_t t0 = timing_mark(s);
             const int li0 = (int)(s->launches % 3);
             const int rc = s->variant == SILT_VARIANT_STRICT
                                ? silt_strict_step1d_cluster(s->args, li0, n, ctas, s->stream)
                                : silt_fast_step1d_cluster(s->args, li0, n, ctas, s->stream);
+            timing_close(s, t0);
             if (rc == 0) {
                 s->launches += n;
                 ++s->kernel_count;
@@ -912,9 +967,11 @@ int silt_solver_step(silt_solver* s, int n) {
                                  : silt_fast_step1d_coop_blocks(s->args.P.shields);
         if ((int)s->step_grid.x <= s->coop_blocks) {
             const int li0 = (int)(s->launches % 3);
+            const cudaEvent_t t0 = timing_mark(s);
             const int rc = s->variant == SILT_VARIANT_STRICT
                                ? silt_strict_step1d_coop(s->args, li0, n, s->step_grid, s->stream)
                                : silt_fast_step1d_coop(s->args, li0, n, s->step_grid, s->stream);
+            timing_close(s, t0);
             if (rc != 0) return fail(SILT_ERR_CUDA, cudaGetErrorString((cudaError_t)rc));
             s->launches += n;
             ++s->kernel_count;
@@ -1450,6 +1507,27 @@ int silt_group_capture_wait(silt_group* g) {
 int silt_group_dt_log(silt_group* g, double* host_out, int64_t n) {
     if (!g || g->strips.empty()) return fail(SILT_ERR_INVALID, "null group");
     return silt_solver_dt_log(g->strips[0], host_out, n);
+}
+
+int silt_solver_timing(silt_solver* s, int enable, double* compute_seconds) {
+    if (!s) return fail(SILT_ERR_INVALID, "null solver");
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    timing_harvest(s);
+    if (compute_seconds) *compute_seconds = s->compute_s;
+    if (enable >= 0) {
+        s->timing_on = enable != 0;
+        s->compute_s = 0;
+    }
+    return SILT_OK;
+}
+
+int silt_group_timing(silt_group* g, int enable, double* per_strip) {
+    if (!g) return fail(SILT_ERR_INVALID, "null group");
+    for (size_t k = 0; k < g->strips.size(); ++k)
+        if (int rc = silt_solver_timing(g->strips[k], enable, per_strip ? per_strip + k : nullptr))
+            return rc;
+    return SILT_OK;
 }
 
 }  // extern "C"

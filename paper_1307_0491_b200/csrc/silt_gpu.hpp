@@ -24,6 +24,7 @@
 //     time as compute_seconds (device work is not attributed per phase).
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -179,6 +180,7 @@ inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
     silt_run_plan plan{t_end, opt.max_steps, opt.snapshot_times.data(),
                        static_cast<int32_t>(opt.snapshot_times.size()), 0};
     check(silt_group_begin(g.get(), &plan));
+    check(silt_group_timing(g.get(), 1, nullptr));  // WorkerTiming.compute_seconds from here
     const auto loop0 = std::chrono::steady_clock::now();
     silt_status st{};
     // Snapshots are gathered asynchronously: the paused state is captured on
@@ -210,6 +212,8 @@ inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
         if (st.state == SILT_STATE_DONE) break;
     }
     deliver();
+    std::vector<double> compute(py, 0.0);
+    check(silt_group_timing(g.get(), 0, compute.data()));
     const double loop_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - loop0).count();
     RunResult res;
@@ -217,11 +221,18 @@ inline RunResult run(const Scenario& sc, int py, const RunOptions& opt) {
     check(silt_group_download(g.get(), data(res.final_field.cells)));
     res.time = st.t;
     res.steps = st.steps;
+    // The reference's split (src/parallel.cpp:318-361): compute = local CFL +
+    // stepping, exchange = ghost fill, gathers and synchronisation.  Here
+    // compute is the strip's step-kernel time on its device (the fused step
+    // includes the next CFL reduction); the rest of the run loop's wall time —
+    // halo delivery, the maxima exchange, waits on the other strips, snapshot
+    // gathers and host round trips — is exchange.
     for (int r = 0; r < py; ++r) {
         WorkerTiming w;
         w.rank = r;
         w.steps = st.steps;
-        w.compute_seconds = loop_s;
+        w.compute_seconds = compute[r];
+        w.exchange_seconds = loop_s > compute[r] ? loop_s - compute[r] : 0.0;
         res.timing.push_back(w);
     }
     res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
@@ -277,7 +288,13 @@ inline RunResult run_parallel(const Scenario& sc, int px, int py, const RunOptio
         throw std::invalid_argument("partition: 1D grids require py == 1");
     if (px > sc.grid.nx || py > sc.grid.ny)
         throw std::invalid_argument("partition: every worker needs at least one cell per axis");
-    return detail::run(sc, py, opt);
+    // The GPU decomposition is row strips: a px x py layout runs as px * py
+    // strips (capped at one row each; a 1D line is one strip).  Every layout
+    // gives the same fields bit for bit (tests/test_parallel.cpp:215-238), so
+    // only the worker count carries over; res.timing has one entry per strip.
+    const long long workers = (long long)px * py;
+    const int strips = sc.grid.dim == 1 ? 1 : (int)std::min<long long>(workers, sc.grid.ny);
+    return detail::run(sc, strips, opt);
 }
 
 }  // namespace gpu

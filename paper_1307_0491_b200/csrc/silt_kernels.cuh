@@ -508,7 +508,11 @@ __device__ __forceinline__ Side side_of(const StepArgs& A, const double c[4], bo
 
 template <bool S, bool SH>
 __device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], Side& sx, Side& sy) {
+#ifdef SILT_FAST_REF_SIDES  // diagnostics: FAST face solver on the reference's per-cell terms
+    if constexpr (true) {
+#else
     if constexpr (S) {
+#endif
         sx = make_side_ref<SH>(A.P, c[0], c[1], c[2], c[3]);
         sy = make_side_ref<SH>(A.P, c[0], c[2], c[1], c[3]);
     } else {

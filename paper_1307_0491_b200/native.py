@@ -92,6 +92,8 @@ def lib() -> C.CDLL:
         "silt_group_status": ([_VP, C.POINTER(SiltStatus)], C.c_int),
         "silt_group_resume": ([_VP], C.c_int),
         "silt_group_dt_log": ([_VP, _D, C.c_int64], C.c_int),
+        "silt_group_timing": ([_VP, C.c_int, _D], C.c_int),
+        "silt_solver_timing": ([_VP, C.c_int, _D], C.c_int),
         "silt_group_capture_resume": ([_VP, _D], C.c_int),
         "silt_group_capture_wait": ([_VP], C.c_int),
         "silt_solver_capture_resume": ([_VP, _D], C.c_int),

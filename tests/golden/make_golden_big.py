@@ -31,11 +31,11 @@ Cases
   C5   BASELINE configs[4]'s generator (scenarios.random_bed_2d) on the per-GPU
        tile 8192 x 4096 (bench.py --workload C5 at N = 1), A_g = 0.01, CFL 0.4,
        100 steps: every face takes the full solver.
-  C4w40_fma / C3_fma
+  C4w40_fma / C4w500_fma / C3_fma
        The reference's own rounding spread: the same reference sources compiled
        with FMA contraction (oracle/_ref/libsilt_ref_fma.so, `make -C oracle
        ref_fma`) against the default build, per field (normwise), on the C4
-       window after 40 steps and on C3 after 1000 steps.  Early in the C4 run hv
+       window after 40 and 500 steps and on C3 after 1000 steps.  Early in the C4 run hv
        is O(1e-7) while the y-momentum fluxes it is the difference of are
        O(500), so its per-field ratio there measures rounding: the reference
        disagrees with itself by ~1e-5 (tests/test_gpu_parity.py uses this as
@@ -117,6 +117,9 @@ def fma_spread(name: str, threads: int):
     if name == "C4w40_fma":
         p, init, win = c4_window_problem(48)
         steps, py = 40, 64
+    elif name == "C4w500_fma":
+        p, init, win = c4_window_problem()
+        steps, py = C4_STEPS, 128
     else:
         p, init, steps = S.dune_2d(1024, steps=1000)
         py = 64
