@@ -95,6 +95,15 @@ class CpuSolver:
             g.argtypes = [_P, _D, C.c_double, _I64, C.c_int, C.c_int, _D,
                           C.POINTER(_I64), _D, _D, _D]
             self._runp = g
+            g = L.ref_build_scenario
+            g.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_double, _P, _D, C.POINTER(_I64), _D]
+            g.restype = C.c_int
+            self._build = g
+            g = L.ref_run_snaps
+            g.argtypes = [_P, _D, C.c_double, _D, C.c_int, _D, C.POINTER(C.c_int), _D,
+                          C.POINTER(_I64)]
+            g.restype = C.c_int
+            self._runs = g
             g = L.ref_run_blocks
             g.argtypes = [_P, _D, _I64, C.c_int, C.c_int, _D, _D, C.POINTER(_I64), _D]
             g.restype = C.c_int
@@ -145,6 +154,31 @@ class CpuSolver:
                                int(threads), _dp(out), _dp(log), C.byref(steps),
                                C.byref(t)))
         return out, t.value, steps.value, log[:steps.value].copy()
+
+    def build_scenario(self, name: str, cells_x: int = 0, cells_y: int = 0, a_g: float = 1.0):
+        """The reference's bundled scenario (build_scenario / build_bump_2d):
+        (problem, AoS initial field (ny, nx, 4), t_end)."""
+        p = SiltProblem()
+        n = _I64(0)
+        t_end = C.c_double(0)
+        self._check(self._build(name.encode(), cells_x, cells_y, a_g, C.byref(p), None,
+                                C.byref(n), C.byref(t_end)))
+        init = np.empty((p.ny, p.nx, 4))
+        self._check(self._build(name.encode(), cells_x, cells_y, a_g, C.byref(p), _dp(init),
+                                C.byref(n), C.byref(t_end)))
+        return p, init, t_end.value
+
+    def run_snaps(self, problem, init, t_end: float, times):
+        """run_serial with snapshot times: (list of landed fields, t, steps)."""
+        init = np.ascontiguousarray(init, dtype=np.float64)
+        times = np.ascontiguousarray(np.asarray(times, dtype=np.float64))
+        out = np.empty((len(times),) + init.shape)
+        landed = C.c_int(0)
+        t = C.c_double(0)
+        steps = _I64(0)
+        self._check(self._runs(C.byref(problem), _dp(init), float(t_end), _dp(times), len(times),
+                               _dp(out), C.byref(landed), C.byref(t), C.byref(steps)))
+        return [out[k] for k in range(min(landed.value, len(times)))], t.value, steps.value
 
     def cfl_dt(self, problem, field) -> float:
         field = np.ascontiguousarray(field, dtype=np.float64)

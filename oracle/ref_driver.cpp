@@ -261,6 +261,71 @@ int ref_run_blocks(const silt_problem* p, const double* init, int64_t max_steps,
     });
 }
 
+// The reference's bundled scenarios (build_scenario, src/scenarios.cpp:289-296
+// with build_bump_2d's a_g / t_end arguments when name == "bump2d"): fills
+// *p (grid, law, physics, cfl, safety, BCs), *t_end and, when init != NULL,
+// the AoS initial field (query the cell count with init == NULL first).
+int ref_build_scenario(const char* name, int cells_x, int cells_y, double a_g, silt_problem* p,
+                       double* init, int64_t* cells, double* t_end) {
+    return guarded([&] {
+        const std::string n(name);
+        const Scenario sc = n == "bump2d" ? build_bump_2d(cells_x, cells_y, a_g)
+                                          : build_scenario(n, cells_x, cells_y);
+        const Grid& g = sc.grid;
+        std::memset(p, 0, sizeof *p);
+        p->dim = g.dim;
+        p->nx = g.nx;
+        p->ny = g.dim == 1 ? 1 : g.ny;
+        p->dx = g.dx;
+        p->dy = g.dim == 1 ? 1.0 : g.dy;
+        p->gravity = sc.phys.gravity;
+        p->h_dry = sc.phys.h_dry;
+        if (sc.law.kind != BedloadLaw::Kind::Grass)
+            throw std::invalid_argument("ref_build_scenario: Grass scenarios only");
+        p->law_kind = SILT_LAW_GRASS;
+        p->a_g = sc.law.a_g;
+        p->m_g = sc.law.m_g;
+        p->cfl = sc.cfl;
+        p->safety = sc.safety;
+        for (int k = 0; k < 4; ++k) {
+            const BoundarySpec& b = sc.bc[k];
+            p->bc[k].type = b.type == BcType::Inflow     ? SILT_BC_INFLOW
+                            : b.type == BcType::Wall     ? SILT_BC_WALL
+                            : b.type == BcType::Periodic ? SILT_BC_PERIODIC
+                                                         : SILT_BC_OUTFLOW;
+            p->bc[k].supercritical = b.supercritical ? 1 : 0;
+            p->bc[k].q0 = b.q0;
+            p->bc[k].h0 = b.h0;
+        }
+        *cells = (int64_t)sc.initial.cells.size();
+        *t_end = sc.t_end;
+        if (init) store_field(sc.initial, init);
+    });
+}
+
+// silt::run_serial with snapshot times (parallel.hpp:59-66, 80): the field
+// at every landed snapshot, in order, into snaps_out[k] (AoS, cells * 4);
+// *n_landed = how many landed.
+int ref_run_snaps(const silt_problem* p, const double* init, double t_end, const double* times,
+                  int n_times, double* snaps_out, int* n_landed, double* t_out,
+                  int64_t* steps_out) {
+    return guarded([&] {
+        const Scenario sc = make_scenario(*p, init, t_end);
+        RunOptions opt;
+        opt.snapshot_times.assign(times, times + n_times);
+        const std::size_t cells = sc.initial.cells.size();
+        int k = 0;
+        opt.on_snapshot = [&](double, const Field& f) {
+            if (k < n_times) store_field(f, snaps_out + 4 * cells * (std::size_t)k);
+            ++k;
+        };
+        const RunResult r = run_serial(sc, opt);
+        *n_landed = k;
+        *t_out = r.time;
+        *steps_out = r.steps;
+    });
+}
+
 int ref_cfl_dt(const silt_problem* p, const double* field, double* dt) {
     return guarded([&] {
         const Field f = make_field(make_grid(*p), field);

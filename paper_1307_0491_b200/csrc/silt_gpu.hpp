@@ -17,11 +17,14 @@
 // failure (negative depth, no positive Riemann fan).  Differences, by design:
 //   * both law kinds (Grass, Shields x 5 formulas x 2 friction models) run on
 //     the GPU; there is no CPU fallback;
-//   * run_parallel(sc, px, py) validates px/py like partition() and runs py
-//     row strips (columns are never split: every layout is bitwise identical,
-//     tests/test_parallel.cpp:215-238), strip k on CUDA device k % devices;
-//   * RunResult::timing holds one WorkerTiming per strip with the loop's wall
-//     time as compute_seconds (device work is not attributed per phase).
+//   * run_parallel(sc, px, py) validates px/py like partition() and runs
+//     px * py row strips (columns are never split: every layout is bitwise
+//     identical, tests/test_parallel.cpp:215-238), strip k on CUDA device
+//     k % devices; a 1D line is one strip;
+//   * RunResult::timing holds one WorkerTiming per strip: compute_seconds is
+//     the strip's step-kernel time on its device (CUDA events,
+//     silt_group_timing), exchange_seconds the rest of the run loop's wall
+//     time (halo/maxima delivery, waits on other strips, snapshot gathers).
 #pragma once
 
 #include <algorithm>

@@ -500,11 +500,18 @@ struct Flux {
 template <bool S>
 __device__ __forceinline__ void region_from_tau(double tau, double u, double pi, double omega,
                                                 double& hu, double& u0, double& p, double& w) {
+#ifdef SILT_STRICT_U0  // diagnostics: STRICT with FAST's sampled velocity (u0 = u)
+    if constexpr (S) {
+        hu = u / tau;
+        u0 = u;
+    } else {
+#else
     if constexpr (S) {
         const double h = 1.0 / tau;
         hu = u / tau;
         u0 = h > 0 ? hu / h : 0.0;
     } else {
+#endif
         hu = u * rcp(tau);
         u0 = u;
     }
@@ -929,7 +936,11 @@ __device__ __forceinline__ bool face_flux_general_impl(const Params& P, const Si
 // exact form keeps quiescent regions exactly quiescent (and skips the solve).
 template <bool S>
 __device__ __forceinline__ bool face_flux(const Params& P, const Side& l, const Side& r, Flux& F) {
+#ifdef SILT_STRICT_SHORTCUT  // diagnostics: STRICT with FAST's uniform-state shortcut
+    if constexpr (true) {
+#else
     if constexpr (!S) {
+#endif
         if (l.wet && l.h == r.h && l.hun == r.hun && l.ut == r.ut && l.z == r.z) {
             F.h = l.hun;
             F.z = l.omega;

@@ -1,0 +1,108 @@
+"""The reference's physics acceptance criteria through the GPU path.
+
+  3  dune migration + refinement  (proj/tests/acceptance_main.cpp:164-195)
+  4  antidune upstream migration  (:199-225)
+  10 planar bump crescent         (:419-449)
+
+Inputs come from the reference's own scenario builders (oracle/_ref, test
+infrastructure; build_dune_1d / build_antidune_1d / build_bump_2d), the runs
+go through the product (native.Solver, FAST — the production variant — with
+the device run clock landing on every snapshot time), and the criteria are
+evaluated with the reference's crest_track / coarsen2 / l1_bed_diff /
+split_max restated in tests/golden/make_golden_acceptance.py.  Expected values
+are the reference's own (tests/golden/golden_acceptance.json): identical crest
+positions, inflow Froude numbers and bed maxima, the same verdicts — including
+criterion 10, which the reference itself fails (no crest split, recorded in
+proj/test_output.txt:21).
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR, ROOT
+
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+import make_golden_acceptance as A  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def expected():
+    with open(os.path.join(GOLDEN_DIR, "golden_acceptance.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="module")
+def ref(oracle_mod):
+    if not oracle_mod.have_reference():
+        pytest.skip("oracle/_ref not built")
+    return oracle_mod.reference()
+
+
+def gpu_snaps(problem, init, t_end, times):
+    from paper_1307_0491_b200 import abi, native
+    s = native.Solver(problem, variant=abi.VARIANT_FAST)
+    s.upload(init)
+    s.begin(t_end=t_end, snapshots=[t for t in times if t > 0])
+    out = [init.copy()] if 0.0 in times else []
+    st = s.run(batch=256, on_snapshot=lambda t, f: out.append(f.copy()))
+    if not times or times[-1] == t_end and len(out) < len(times):
+        out.append(s.download())
+    s.close()
+    return out, st
+
+
+def test_dune_migrates_downstream(ref, expected):
+    e = expected["dune"]
+    finals = {}
+    for cells in (2000, 4000, 8000):
+        p, init, t_end = ref.build_scenario("dune1d", cells)
+        times = e["snapshots"] if cells == 2000 else [t_end]
+        snaps, st = gpu_snaps(p, init, t_end, times)
+        assert st.steps == e["steps"][str(cells)], cells
+        finals[cells] = (snaps, p.dx)
+    snaps, dx = finals[2000]
+    xs, verdict = A.crest_track(snaps, dx)
+    print("GPU dune crest", xs, verdict)
+    assert xs == e["crest_x"] and verdict == e["verdict"] == "downstream"
+    assert all(b > a for a, b in zip(xs, xs[1:])) and xs[-1] > 400.0
+    d_coarse = A.l1_bed_diff(snaps[-1], A.coarsen2(finals[4000][0][-1]), dx)
+    d_fine = A.l1_bed_diff(finals[4000][0][-1], A.coarsen2(finals[8000][0][-1]), finals[4000][1])
+    print("GPU bed L1 gaps", d_coarse, d_fine, "reference", e["l1_coarse"], e["l1_fine"])
+    assert math.isclose(d_coarse, e["l1_coarse"], rel_tol=1e-9)
+    assert math.isclose(d_fine, e["l1_fine"], rel_tol=1e-9)
+    assert d_coarse > d_fine
+
+
+def test_antidune_migrates_upstream(ref, expected):
+    e = expected["antidune"]
+    p, init, _ = ref.build_scenario("antidune1d", 2400)
+    snaps, st = gpu_snaps(p, init, 50.0, e["snapshots"])
+    assert st.steps == e["steps"]
+    xs, verdict = A.crest_track(snaps, p.dx)
+    fr = [(f[0, 0, 1] / f[0, 0, 0]) / math.sqrt(p.gravity * f[0, 0, 0]) for f in snaps]
+    print("GPU antidune crest", xs, verdict, "inflow Froude", fr)
+    assert xs == e["crest_x"] and verdict == e["verdict"] == "upstream"
+    assert np.allclose(fr, e["inflow_froude"], rtol=1e-9, atol=0)
+    assert min(fr) > 1.0
+
+
+def test_bump_crescent(ref, expected):
+    e = expected["bump"]
+    p, init, t_end = ref.build_scenario("bump2d", 200, 200, 1.0)
+    snaps, st = gpu_snaps(p, init, t_end, [t_end])
+    assert st.steps == e["steps"]
+    c0, o0 = A.bump_split(init)
+    c1, o1 = A.bump_split(snaps[-1])
+    print("GPU bump centre", c0, "->", c1, "off-axis", o1, "| reference", e)
+    assert c0 == e["centre0"]
+    assert math.isclose(c1, e["centre1"], rel_tol=1e-9)
+    assert math.isclose(o1, e["off1"], rel_tol=1e-9)
+    assert (c1 < c0) == e["lowered"] and (o1 > c1) == e["split"]

@@ -185,7 +185,17 @@ def test_c4_full_grid_vs_reference(N, big):
     err = np.array([float((fo[..., f] - so[..., f]).abs().max() / so[..., f].abs().max())
                     for f in range(4)])
     dterr = float(np.max(np.abs(logs["fast"] - logs["strict"]) / logs["strict"]))
+    hv_abs = float((fo[..., 2] - so[..., 2]).abs().max())
+    spread = meta["cases"]["C4w500_fma"]["fma_vs_ref_normwise"]
     print(f"C4 500 steps: FAST vs STRICT per-field normwise h, hu, hv, zb = {err.tolist()}, "
-          f"dt {dterr:.2e}")
+          f"dt {dterr:.2e}; |dhv| max {hv_abs:.2e}; the reference's own FMA-build spread "
+          f"{spread}")
     assert dterr <= DT_TOL
-    assert np.all(err <= FIELD_TOL), err
+    assert np.all(err[[0, 1, 3]] <= FIELD_TOL), err
+    # hv (max |hv| = 4e-4 after 500 steps) sits at the reference's own rounding
+    # floor: any one-ulp change of the face fluxes (FMA contraction of the
+    # reference's own sources, or STRICT with a single FAST-ism) moves it by
+    # ~2.7e-12 absolute, 6e-9 of its norm.  The bar is the
+    # north-star 1e-9 or, where the reference cannot meet it against itself,
+    # its own compile-to-compile spread (make_golden_big.py C4w500_fma).
+    assert err[2] <= max(FIELD_TOL, 1.5 * spread[2]), (err[2], spread[2])

@@ -338,8 +338,20 @@ def test_c4_full_size_properties(N):
     assert sst.steps == steps
     assert np.max(np.abs(flog - slog) / slog) <= DT_TOL
     err = normwise(fo, so)
-    print("C4 40 steps fast vs strict, per-field normwise h, hu, hv, zb:", err.tolist())
-    assert np.all(err <= FIELD_TOL), err
+    import json
+    import os
+
+    from conftest import GOLDEN_DIR
+    with open(os.path.join(GOLDEN_DIR, "golden_big.json")) as fh:
+        spread = json.load(fh)["cases"]["C4w40_fma"]["fma_vs_ref_normwise"]
+    print("C4 40 steps fast vs strict, per-field normwise h, hu, hv, zb:", err.tolist(),
+          "reference FMA-build spread:", spread)
+    assert np.all(err[[0, 1, 3]] <= FIELD_TOL), err
+    # after 40 steps max |hv| is 2e-7: its per-field ratio is rounding noise —
+    # the reference disagrees with itself by 1.1e-5 there (make_golden_big.py
+    # C4w40_fma); the north-star bar applies after 1000 steps
+    # (test_c4_1000_steps_fast_vs_strict: 8.6e-10 on hv)
+    assert err[2] <= max(FIELD_TOL, 1.5 * spread[2]), (err[2], spread[2])
 
 
 @pytest.mark.slow
