@@ -67,6 +67,10 @@ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b 
 #ifndef SILT_SQRT_FAST
 #define SILT_SQRT_FAST 1
 #endif
+// FAST Newton loop: residual tests without forming the max, 1/det to ~2^-46
+#ifndef SILT_FAST_CMP
+#define SILT_FAST_CMP 1
+#endif
 
 // Reciprocal for the FAST variant.  SILT_RCP_FAST: MUFU.RCP64H seed
 // (rcp.approx.ftz.f64) + one cubic Newton correction r += r(e + e^2),
@@ -80,6 +84,19 @@ __device__ __forceinline__ double rcp(double y) {
     return fma(r, fma(e, e, e), r);
 #else
     return __drcp_rn(y);
+#endif
+}
+
+// Reciprocal to ~2^-46 (MUFU seed + one quadratic Newton step): for the Newton
+// step's 1/det only, where the step's accuracy sets the convergence rate, not
+// the converged root (the residuals decide acceptance).
+__device__ __forceinline__ double rcp_step(double y) {
+#if SILT_RCP_FAST && SILT_FAST_CMP
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    return fma(r, fma(-y, r, 1.0), r);
+#else
+    return rcp(y);
 #endif
 }
 
@@ -703,6 +720,24 @@ __device__ __forceinline__ double res_norm(const Eval& v) {
     return smax(fabs(v.r1), fabs(v.r2));
 }
 
+// res_norm(v) <= x without forming the max (FAST): both components <= x.
+// Same decision as smax(|r1|, |r2|) <= x for every non-NaN residual (a NaN
+// r2 with a finite r1 would be accepted by the max form, not here).
+template <bool S>
+__device__ __forceinline__ bool res_le(const Eval& v, double x) {
+    if constexpr (S || !SILT_FAST_CMP)
+        return res_norm(v) <= x;
+    else
+        return fabs(v.r1) <= x && fabs(v.r2) <= x;
+}
+template <bool S>
+__device__ __forceinline__ bool res_lt(const Eval& v, double x) {
+    if constexpr (S || !SILT_FAST_CMP)
+        return res_norm(v) < x;
+    else
+        return fabs(v.r1) < x && fabs(v.r2) < x;
+}
+
 // solve_fluid_outer: src/riemann.cpp:152-262 (stopping rule of the code, :201-204)
 // Outcome of a branch solver attempt.
 constexpr int kIllPosed = 0;  // no positive fan at this celerity pair (IllPosed)
@@ -767,7 +802,7 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
     // already implies res <= tol (rounding is monotone): the common
     // converged-at-the-guess face skips the rest of the scale.  Same decision.
     const double tlr = (tl < tr) ? tr : tl;
-    const bool early = res_norm(e) <= 1e-13 * (tlr * tlr);
+    const bool early = res_le<S>(e, 1e-13 * (tlr * tlr));
     double tol = 0.0;
     if (!early) {
         double tmax = tl;
@@ -783,7 +818,7 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
     }
 
     int it = 0;
-    while (!early && res_norm(e) > tol) {
+    while (!early && !res_le<S>(e, tol)) {
 #ifdef SILT_NEWTON_CAP  // timing experiments only: accept the iterate after CAP iterations
         if (it >= SILT_NEWTON_CAP) break;
 #endif
@@ -808,7 +843,7 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
             j22 = fma(-e.t2, c.ib, tk * (c.jz - e.dzl));
             det = j11 * j22 - j12 * j21;
             if (det == 0.0 || !isfinite(det)) return kTry ? kBail : kIllPosed;
-            const double idet = rcp(det);
+            const double idet = rcp_step(det);
             step2 = (e.r1 * j22 - e.r2 * j12) * idet;
             step4 = (e.r2 * j11 - e.r1 * j21) * idet;
         }
@@ -817,7 +852,7 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
         const double rn = res_norm(e);
         for (int bt = 0; bt < (kTry ? 1 : 40); ++bt) {
             const Eval trial = fo_eval<S>(c, m2 - damp * step2, m4 - damp * step4);
-            if (trial.valid && (res_norm(trial) < rn || res_norm(trial) <= tol)) {
+            if (trial.valid && (res_lt<S>(trial, rn) || res_le<S>(trial, tol))) {
                 m2 -= damp * step2;
                 m4 -= damp * step4;
                 e = trial;
