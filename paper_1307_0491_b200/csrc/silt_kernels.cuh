@@ -320,6 +320,70 @@ __device__ __forceinline__ void reduce_fold(const StepArgs& A, Reduce& R, const 
     }
 }
 
+#ifndef SILT_FAST_SPEEDFILTER
+#define SILT_FAST_SPEEDFILTER 1
+#endif
+
+// CFL speeds of an updated row (the NEXT step's cfl_dt), folded into the
+// lane's maxima.  Warp-collective (every lane calls it; `upd`: this lane
+// updated a cell).  FAST + Grass m_g = 3 with a_g >= 0: only the warp's
+// maxima matter, so each cell's speeds are first estimated in fp32 (~1e-6
+// relative) and evaluated exactly (fp64) only when the estimate comes within
+// 1e-4 of the warp's running maximum `thr` (rounded down to float) — a cell
+// below it cannot change the maxima.  The result is bit-identical to folding
+// every cell; hmax and the wet flag see every cell.
+template <bool S, bool SH>
+__device__ __forceinline__ void fold_speeds(const StepArgs& A, Reduce& R, const double o[4], bool upd,
+                                            float& thr_x, float& thr_y) {
+    const Params& P = A.P;
+    bool filter = false;
+    if constexpr (!S && !SH && SILT_FAST_SPEEDFILTER) filter = P.m3 && P.a_g >= 0.0 && A.dim == 2;
+    if (!filter) {
+        if (upd) {
+            double sx, sy;
+            cell_speeds<S, SH>(A, o, sx, sy);
+            reduce_fold(A, R, o, sx, sy);
+        }
+        return;
+    }
+    bool cand = false;
+    if (upd) {
+        R.hmax = smax(R.hmax, o[0]);
+        if (o[0] > P.h_dry) {
+            R.wet = 1u;
+            const float hf = (float)o[0];
+            const float ih = __frcp_rn(hf);
+            const float uf = (float)o[1] * ih, vf = (float)o[2] * ih;
+            const float g = (float)P.g, ag = (float)P.a_g;
+            const float uu = uf * uf, vv = vf * vf;
+            const bool on = uu + vv > 1e-20f;
+            const float dqx = on ? ag * (3.0f * uu + vv) : 0.0f;
+            const float dqy = on ? ag * (3.0f * vv + uu) : 0.0f;
+            const float gh = g * hf;
+            const float sxf = fabsf(uf) + sqrtf(fmaxf(gh, uu + g * dqx));
+            const float syf = fabsf(vf) + sqrtf(fmaxf(gh, vv + g * dqy));
+            // NaN / inf estimates are candidates
+            cand = !(sxf * 1.0001f < thr_x) || !(syf * 1.0001f < thr_y);
+        }
+    }
+    if (__any_sync(0xffffffffu, cand)) {
+        if (cand) {
+            double sx, sy;
+            cell_speeds<S, SH>(A, o, sx, sy);
+            if (sx == sx) R.sx = smax(R.sx, sx);
+            if (sy == sy) R.sy = smax(R.sy, sy);
+        }
+        double mx = R.sx, my = R.sy;
+#pragma unroll
+        for (int k = 16; k > 0; k >>= 1) {
+            mx = smax(mx, __shfl_xor_sync(0xffffffffu, mx, k));
+            my = smax(my, __shfl_xor_sync(0xffffffffu, my, k));
+        }
+        thr_x = __double2float_rd(mx);
+        thr_y = __double2float_rd(my);
+    }
+}
+
 // warp reduce + one conditional atomic per warp into the slot
 __device__ __forceinline__ void reduce_flush(Reduce R, Slot& s) {
 #pragma unroll
@@ -601,6 +665,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     // skipped row of a streak), folded into the reduction once per streak.
     bool quiet_prev = false, qvalid = false;
     double qsx = 0.0, qsy = 0.0;
+    float thr_x = 0.0f, thr_y = 0.0f;  // fold_speeds: the warp's running maxima (rounded down)
     // streak loop (below): not in the warps holding an x-ghost column, whose
     // ghost cells are transformed after the load
     const bool xedge = i0 == 0 || i0 + kCellsPerWarp >= A.nx;
@@ -742,26 +807,26 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             }
             side_to_ring(sh_side, sm.side_fl, sy, t);
         }
+        double o[4];
+        bool upd = false;
         if (r - 1 >= jb && owned) {
             // y update of row r-1 (src/stepper.cpp:181-186) + check_depth
-            double o[4];
             o[0] = sh_xs[0][t] - cy * (fy.h - sh_fy[0][t]);
             o[2] = sh_xs[2][t] - cy * (fy.huL - sh_fy[1][t]);
             o[1] = sh_xs[1][t] - cy * (fy.hv - sh_fy[2][t]);
             o[3] = sh_xs[3][t] - cy * (fy.z - sh_fy[3][t]);
             if (!check_depth(o[0], href)) record_error(A, kErrNegDepth, col, r - 1 + A.j0, nullptr, nxt);
-            if (SILT_VIOLATED(r - 1 >= 0 && r - 1 < A.ny && col >= 0 && col < A.nx, 5, r - 1, col))
-                continue;
-            const size_t off = (size_t)(r - 1) * A.pitch;
-            out0[off] = o[0];
-            out0[off + plane] = o[1];
-            out0[off + 2 * plane] = o[2];
-            out0[off + 3 * plane] = o[3];
-            if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, o);
-            double ssx, ssy;
-            cell_speeds<S, SH>(A, o, ssx, ssy);
-            reduce_fold(A, R, o, ssx, ssy);
+            if (!SILT_VIOLATED(r - 1 >= 0 && r - 1 < A.ny && col >= 0 && col < A.nx, 5, r - 1, col)) {
+                const size_t off = (size_t)(r - 1) * A.pitch;
+                out0[off] = o[0];
+                out0[off + plane] = o[1];
+                out0[off + 2 * plane] = o[2];
+                out0[off + 3 * plane] = o[3];
+                if (r - 1 == 0 || r - 1 == A.ny - 1) write_edges(A, q, col, r - 1, o);
+                upd = true;
+            }
         }
+        if (r - 1 >= jb) fold_speeds<S, SH>(A, R, o, upd, thr_x, thr_y);  // warp-uniform
         if (!own_row) continue;  // warp-uniform
         sh_fy[0][t] = fy.h;
         sh_fy[1][t] = fy.huR;

@@ -71,6 +71,10 @@ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b 
 #ifndef SILT_FAST_CMP
 #define SILT_FAST_CMP 1
 #endif
+// FAST fluid-outer evaluation without the early exit, tmax on the integer pipe
+#ifndef SILT_FAST_BRANCHFREE
+#define SILT_FAST_BRANCHFREE 1
+#endif
 
 // Reciprocal for the FAST variant.  SILT_RCP_FAST: MUFU.RCP64H seed
 // (rcp.approx.ftz.f64) + one cubic Newton correction r += r(e + e^2),
@@ -678,6 +682,7 @@ struct Eval {
 
 struct FluidCtx {
     double lam, rho, amb, iamb, b, ib, i2b, kappa, jz, jw, k;
+    double k2, k2jz;  // FAST: 2k and 2k jz (loop invariants of the residuals)
 };
 
 template <bool S>
@@ -697,8 +702,12 @@ __device__ __forceinline__ Eval fo_eval(const FluidCtx& c, double m2, double m4)
     }
     e.d = m4 - m2;
     e.valid = e.t1 > 0 && e.t2 > 0 && e.t3 > 0 && e.t4 > 0 && e.d > 0;
-    // the other fields of an invalid evaluation are never read
-    if (!e.valid) return e;
+    // the other fields of an invalid evaluation are never read.  STRICT
+    // returns at once (the reference's order); FAST evaluates them anyway,
+    // branch-free, so 1/d and the residuals start alongside the validity test
+    if constexpr (S || !SILT_FAST_BRANCHFREE) {
+        if (!e.valid) return e;
+    }
     if constexpr (S) {
         e.dzl = (m4 * c.jz - c.jw) / e.d;
         e.dzr = (m2 * c.jz - c.jw) / e.d;
@@ -710,8 +719,8 @@ __device__ __forceinline__ Eval fo_eval(const FluidCtx& c, double m2, double m4)
         e.dzr = 0.0;  // FAST: derived as dzl - jz where needed
         const double q12 = (e.t1 - e.t2) * (e.t1 + e.t2);
         const double q34 = (e.t3 - e.t4) * (e.t3 + e.t4);
-        e.r1 = q12 + q34 + 2.0 * c.k * c.jz;
-        e.r2 = q12 + 2.0 * c.k * e.dzl;
+        e.r1 = q12 + q34 + c.k2jz;
+        e.r2 = fma(c.k2, e.dzl, q12);
     }
     return e;
 }
@@ -776,6 +785,8 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
         const double a2 = a * a;
         const double ia = rcp(a);
         c.k = g * rcp(fma(a, a, -b * b));
+        c.k2 = 2.0 * c.k;
+        c.k2jz = c.k2 * (r.z - l.z);
         kl = fma(a2, tl, l.pi);
         kr = fma(a2, tr, r.pi);
         c.kappa = (kr - kl) * (ia * ia);
@@ -805,12 +816,23 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
     const bool early = res_le<S>(e, 1e-13 * (tlr * tlr));
     double tol = 0.0;
     if (!early) {
-        double tmax = tl;
-        tmax = (tmax < tr) ? tr : tmax;
-        tmax = (tmax < e.t1) ? e.t1 : tmax;
-        tmax = (tmax < e.t2) ? e.t2 : tmax;
-        tmax = (tmax < e.t3) ? e.t3 : tmax;
-        tmax = (tmax < e.t4) ? e.t4 : tmax;
+        double tmax;
+        if constexpr (S || !SILT_FAST_BRANCHFREE) {
+            tmax = tl;
+            tmax = (tmax < tr) ? tr : tmax;
+            tmax = (tmax < e.t1) ? e.t1 : tmax;
+            tmax = (tmax < e.t2) ? e.t2 : tmax;
+            tmax = (tmax < e.t3) ? e.t3 : tmax;
+            tmax = (tmax < e.t4) ? e.t4 : tmax;
+        } else {
+            // all six are positive finite doubles (tau_of > 0, a valid fan):
+            // their bit patterns order like the values, so the max runs on
+            // the integer pipe (same result)
+            long long m = max(__double_as_longlong(tl), __double_as_longlong(tr));
+            m = max(m, max(__double_as_longlong(e.t1), __double_as_longlong(e.t2)));
+            m = max(m, max(__double_as_longlong(e.t3), __double_as_longlong(e.t4)));
+            tmax = __longlong_as_double(m);
+        }
         const double dzr = S ? e.dzr : e.dzl - c.jz;  // FAST: dzl - dzr == jz
         const double res_scale = tmax * tmax + fabs(2.0 * c.k * c.jz) +
                                  fabs(2.0 * c.k * e.dzl) + fabs(2.0 * c.k * dzr);
@@ -836,7 +858,7 @@ __device__ __forceinline__ int solve_fluid_outer(const Side& l, const Side& r, d
         } else {
             const double kib = c.kappa * c.ib;
             const double t1a = 2.0 * e.t1 * c.iamb;
-            const double tk = 2.0 * c.k * e.id;
+            const double tk = c.k2 * e.id;
             j11 = t1a - kib;
             j12 = fma(2.0 * e.t4, c.iamb, kib);
             j21 = fma(e.t2, c.ib, fma(tk, e.dzl, t1a));
