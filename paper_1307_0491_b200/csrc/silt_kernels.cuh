@@ -320,67 +320,17 @@ __device__ __forceinline__ void reduce_fold(const StepArgs& A, Reduce& R, const 
     }
 }
 
-#ifndef SILT_FAST_SPEEDFILTER
-#define SILT_FAST_SPEEDFILTER 1
-#endif
-
 // CFL speeds of an updated row (the NEXT step's cfl_dt), folded into the
-// lane's maxima.  Warp-collective (every lane calls it; `upd`: this lane
-// updated a cell).  FAST + Grass m_g = 3 with a_g >= 0: only the warp's
-// maxima matter, so each cell's speeds are first estimated in fp32 (~1e-6
-// relative) and evaluated exactly (fp64) only when the estimate comes within
-// 1e-4 of the warp's running maximum `thr` (rounded down to float) — a cell
-// below it cannot change the maxima.  The result is bit-identical to folding
-// every cell; hmax and the wet flag see every cell.
+// lane's maxima.  (An fp32-screened fold — exact fp64 speeds only for cells
+// whose fp32 estimate reaches the warp's running maximum — was bit-identical
+// but measured 7 % slower on C5: DESIGN.md §7.)
 template <bool S, bool SH>
-__device__ __forceinline__ void fold_speeds(const StepArgs& A, Reduce& R, const double o[4], bool upd,
-                                            float& thr_x, float& thr_y) {
-    const Params& P = A.P;
-    bool filter = false;
-    if constexpr (!S && !SH && SILT_FAST_SPEEDFILTER) filter = P.m3 && P.a_g >= 0.0 && A.dim == 2;
-    if (!filter) {
-        if (upd) {
-            double sx, sy;
-            cell_speeds<S, SH>(A, o, sx, sy);
-            reduce_fold(A, R, o, sx, sy);
-        }
-        return;
-    }
-    bool cand = false;
+__device__ __forceinline__ void fold_speeds(const StepArgs& A, Reduce& R, const double o[4],
+                                            bool upd) {
     if (upd) {
-        R.hmax = smax(R.hmax, o[0]);
-        if (o[0] > P.h_dry) {
-            R.wet = 1u;
-            const float hf = (float)o[0];
-            const float ih = __frcp_rn(hf);
-            const float uf = (float)o[1] * ih, vf = (float)o[2] * ih;
-            const float g = (float)P.g, ag = (float)P.a_g;
-            const float uu = uf * uf, vv = vf * vf;
-            const bool on = uu + vv > 1e-20f;
-            const float dqx = on ? ag * (3.0f * uu + vv) : 0.0f;
-            const float dqy = on ? ag * (3.0f * vv + uu) : 0.0f;
-            const float gh = g * hf;
-            const float sxf = fabsf(uf) + sqrtf(fmaxf(gh, uu + g * dqx));
-            const float syf = fabsf(vf) + sqrtf(fmaxf(gh, vv + g * dqy));
-            // NaN / inf estimates are candidates
-            cand = !(sxf * 1.0001f < thr_x) || !(syf * 1.0001f < thr_y);
-        }
-    }
-    if (__any_sync(0xffffffffu, cand)) {
-        if (cand) {
-            double sx, sy;
-            cell_speeds<S, SH>(A, o, sx, sy);
-            if (sx == sx) R.sx = smax(R.sx, sx);
-            if (sy == sy) R.sy = smax(R.sy, sy);
-        }
-        double mx = R.sx, my = R.sy;
-#pragma unroll
-        for (int k = 16; k > 0; k >>= 1) {
-            mx = smax(mx, __shfl_xor_sync(0xffffffffu, mx, k));
-            my = smax(my, __shfl_xor_sync(0xffffffffu, my, k));
-        }
-        thr_x = __double2float_rd(mx);
-        thr_y = __double2float_rd(my);
+        double sx, sy;
+        cell_speeds<S, SH>(A, o, sx, sy);
+        reduce_fold(A, R, o, sx, sy);
     }
 }
 
@@ -665,7 +615,6 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     // skipped row of a streak), folded into the reduction once per streak.
     bool quiet_prev = false, qvalid = false;
     double qsx = 0.0, qsy = 0.0;
-    float thr_x = 0.0f, thr_y = 0.0f;  // fold_speeds: the warp's running maxima (rounded down)
     // streak loop (below): not in the warps holding an x-ghost column, whose
     // ghost cells are transformed after the load
     const bool xedge = i0 == 0 || i0 + kCellsPerWarp >= A.nx;
@@ -826,7 +775,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                 upd = true;
             }
         }
-        if (r - 1 >= jb) fold_speeds<S, SH>(A, R, o, upd, thr_x, thr_y);  // warp-uniform
+        fold_speeds<S, SH>(A, R, o, upd);
         if (!own_row) continue;  // warp-uniform
         sh_fy[0][t] = fy.h;
         sh_fy[1][t] = fy.huR;
