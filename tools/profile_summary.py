@@ -83,6 +83,26 @@ def full(rep):
     return name, res
 
 
+def opcode_mix(rep):
+    """Dynamic mix: executed warp instructions per SASS opcode (ncu's
+    sass__inst_executed_per_opcode, instance names = opcodes)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--metrics",
+                          "sass__inst_executed_per_opcode", "--print-metric-instances", "details"],
+                         capture_output=True, text=True).stdout
+    flat = " ".join(out.split())
+    i = flat.find("sass__inst_executed_per_opcode")
+    if i < 0 or "(" not in flat[i:]:
+        return []
+    body = flat[flat.index("(", i) + 1:]
+    body = body[:body.index(")")]
+    mix = []
+    for item in body.split(";"):
+        if ":" in item:
+            op, v = item.split(":")
+            mix.append((op.strip(), int(v.strip())))
+    return sorted(mix, key=lambda x: -x[1])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
@@ -127,6 +147,21 @@ def main():
                          "source": os.path.basename(a.out) + "_full.md"}
                 tj[a.workload] = entry
                 json.dump(tj, open(tp, "w"), indent=1)
+            mix = opcode_mix(a.full)
+            if mix:
+                tot = sum(v for _, v in mix)
+                fp64 = sum(v for op, v in mix if op in ("DFMA", "DMUL", "DADD", "DSETP"))
+                fh.write("\nDynamic instruction mix (executed warp instructions per SASS opcode, "
+                         "`sass__inst_executed_per_opcode`)")
+                if a.cells:
+                    fh.write(f"; per cell-update = count / {int(a.cells)} x 32 lanes")
+                fh.write(f".  FP64 pipe (DFMA+DMUL+DADD+DSETP): {100 * fp64 / tot:.1f}% of "
+                         "all instructions.\n\n| opcode | warp instructions | share |"
+                         + (" per cell-update |" if a.cells else "") + "\n|---|---|---|"
+                         + ("---|" if a.cells else "") + "\n")
+                for op, v in mix[:24]:
+                    fh.write(f"| {op} | {v} | {100 * v / tot:.1f}% |"
+                             + (f" {32 * v / a.cells:.1f} |" if a.cells else "") + "\n")
 
 
 if __name__ == "__main__":
