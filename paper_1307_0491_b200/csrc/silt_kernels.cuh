@@ -549,10 +549,6 @@ struct StepSmem {
     int nfull[kStepThreads / 32];         // full-path rows of each warp (launch order)
 };
 
-#ifndef SILT_ONE_FACE_SITE
-#define SILT_ONE_FACE_SITE 0
-#endif
-
 // Rows of a warp's march on the full (non-quiescent) path above which its
 // row block counts as hot for the next launch's order.
 constexpr int kHotRows = 4;
@@ -747,39 +743,6 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         // y face between rows r-1 and r (normal = v, transverse = u), solved
         // first; the x-side waits in shared memory for the x face
         Flux fy{0, 0, 0, 0, 0};
-#if SILT_ONE_FACE_SITE
-        // Both faces through ONE inlined copy of the face solver (a 2-trip
-        // loop): half the code of the two call sites
-        Flux fx{0, 0, 0, 0, 0};
-        {
-            Side sx, sy;
-            sides_of<S, SH>(A, c, sx, sy);
-            if (own_row) side_to_ring(sh_sx, sm.sx_fl, sx, t);
-            __syncwarp();  // the right neighbour's x side is in shared memory
-#pragma unroll 1
-            for (int k = 0; k < 2; ++k) {
-                const bool act = k == 0 ? (r > jb - 1 && owned) : (own_row && xface);
-                Side L, Rs;
-                if (k == 0) {
-                    L = side_from_ring(sh_side, sm.side_fl, t);
-                    Rs = sy;
-                } else {
-                    L = side_from_ring(sh_sx, sm.sx_fl, t);
-                    Rs = side_from_ring(sh_sx, sm.sx_fl, t + 1);
-                }
-                Flux F{0, 0, 0, 0, 0};
-                if (act && !face_flux<S>(A.P, L, Rs, F)) {
-                    const double info[6] = {L.h, L.un, L.z, Rs.h, Rs.un, Rs.z};
-                    record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
-                }
-                if (k == 0)
-                    fy = F;
-                else
-                    fx = F;
-            }
-            side_to_ring(sh_side, sm.side_fl, sy, t);
-        }
-#else
         {
             Side sx, sy;
             sides_of<S, SH>(A, c, sx, sy);
@@ -793,7 +756,6 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
             }
             side_to_ring(sh_side, sm.side_fl, sy, t);
         }
-#endif
         double o[4];
         bool upd = false;
         if (r - 1 >= jb && owned) {
@@ -819,7 +781,6 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         sh_fy[1][t] = fy.huR;
         sh_fy[2][t] = fy.hv;
         sh_fy[3][t] = fy.z;
-#if !SILT_ONE_FACE_SITE
         __syncwarp();
         // x faces: this lane solves the face between col and col+1
         Flux fx{0, 0, 0, 0, 0};
@@ -831,7 +792,6 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                 record_error(A, kErrRiemann, col, r + A.j0, info, nxt);
             }
         }
-#endif
         const double lh = shfl_up_d(fx.h, 1), lhuR = shfl_up_d(fx.huR, 1);
         const double lhv = shfl_up_d(fx.hv, 1), lz = shfl_up_d(fx.z, 1);
         // x update (step_2d x sweep, src/stepper.cpp:165-170)

@@ -351,6 +351,13 @@ class Solver:
     def capture_wait(self):
         check(self.L.silt_solver_capture_wait(self.h))
 
+    def capture_query(self) -> bool:
+        """True once the last capture (device copy, or a background CSV write)
+        has fully landed; raises the background writer's error."""
+        landed = C.c_int(0)
+        check(self.L.silt_solver_capture_query(self.h, C.byref(landed)))
+        return bool(landed.value)
+
     def capture_write(self, time: float, path: str, append: bool = False):
         """CSV snapshot of a paused run, written in the background while the run
         continues (silt_solver_capture_write); capture_wait() joins it."""

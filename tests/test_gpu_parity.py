@@ -183,6 +183,31 @@ def test_step_padded_caller_dt_as_given(N, restatement, variant):
         N.step_padded(p, pd, float("nan"), v)
 
 
+@pytest.mark.parametrize("first", [3, 4])
+@pytest.mark.parametrize("variant", ["strict", "fast"])
+def test_begin_again_continues_from_current_state(N, golden, first, variant):
+    """A second silt_solver_begin without a new upload starts a new run from
+    the CURRENT state whatever the parity of the steps taken (state n lives in
+    the odd plane set after an odd count): `first` steps, begin, 2 more steps
+    equal first + 2 steps in one run, bit for bit."""
+    data, meta = golden
+    case = "rand48x32"
+    p = problem_from_meta(meta["cases"][case])
+    init = data[f"{case}_init"]
+    v = VARIANTS[variant]
+    one, _, n1, _ = N.run(p, init, max_steps=first + 2, variant=v)
+    s = N.Solver(p, variant=v)
+    s.upload(init)
+    s.begin(max_steps=first)
+    st = s.run(batch=1)
+    assert st.steps == first
+    s.begin(max_steps=2)
+    st = s.run(batch=1)
+    assert st.steps == 2
+    assert np.array_equal(s.download(), one)
+    s.close()
+
+
 def test_snapshots_pause_and_land(N, golden):
     """Snapshot landing (run_parallel snapshot clipping, src/parallel.cpp:333-363):
     the device clock pauses exactly on each requested time."""

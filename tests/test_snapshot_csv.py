@@ -209,3 +209,42 @@ def test_gpu_async_csv_snapshots(N, restatement, golden, tmp_path):
     ref, rt, n, _ = restatement.run(p, init, max_steps=m["max_steps"] + len(snaps),
                                     snapshots=snaps)
     assert st.steps == n and np.array_equal(final, ref)
+
+
+@pytest.mark.gpu
+def test_gpu_capture_query_waits_for_the_writer(N, restatement, golden, tmp_path):
+    """silt_solver_capture_query reports a background CSV snapshot as landed
+    only once the file is completely written (then its bytes are final), and
+    reports the writer's error (an unwritable path) instead of 'landed'."""
+    import time
+    data, meta = golden
+    m = meta["cases"]["rand48x32"]
+    p = problem_from_meta(m)
+    init = data["rand48x32_init"]
+    T = m["t_final"]
+    s = N.Solver(p, variant=abi.VARIANT_STRICT)
+    s.upload(init)
+    s.begin(max_steps=m["max_steps"] + 2, snapshots=[0.3 * T, 0.7 * T])
+    paths = [tmp_path / "a.csv", tmp_path / "missing_dir" / "b.csv"]
+    results = []
+    while True:
+        s.step(4)
+        st = s.status()
+        if st.state == abi.STATE_PAUSED:
+            k = len(results)
+            field = s.download()
+            s.capture_write(st.t, str(paths[k]))
+            try:
+                while not s.capture_query():
+                    time.sleep(0.0005)
+                results.append(("landed", st.t, field, paths[k].read_bytes()))
+            except N.SiltRuntimeError as e:
+                results.append(("error", st.t, field, str(e)))
+            continue
+        if st.state == abi.STATE_DONE:
+            break
+    s.capture_wait()
+    s.close()
+    kind, t, field, got = results[0]
+    assert kind == "landed" and got == restatement.snapshot_to_string(p, field, t)
+    assert results[1][0] == "error"
