@@ -341,8 +341,9 @@ def main():
 
     import torch
     from paper_1307_0491_b200 import abi, native
-    from paper_1307_0491_b200.distributed import (StripRunner, balanced_partition, init_dist,
-                                                  refine_partition, row_costs)
+    from paper_1307_0491_b200.distributed import (PieceRunner, StripRunner, balanced_partition,
+                                                  init_dist, piece_partition, refine_partition,
+                                                  row_costs)
 
     world, rank, local = init_dist(args.gpus)
     # one GPU per rank; ranks beyond the visible devices share them (only for
@@ -353,16 +354,26 @@ def main():
     variant = abi.VARIANT_FAST if args.variant == "fast" else abi.VARIANT_STRICT
     p = build_global_problem(args.workload, world, args.law)
     partition = None
+    layout = None  # two pieces per rank (PieceRunner)
     if world > 1 and args.partition == "balanced" and WORKLOADS[args.workload]["kind"] == "dune":
-        # Work-balanced row strips (quiescent rows are cheaper).  Every rank
-        # derives the same cut from the same initial field; a short untimed
-        # pilot then rescales the model by each strip's measured step time.
+        # Work-balanced layouts (quiescent rows are cheaper).  Every rank
+        # derives the same cut from the same initial field.  Default: two
+        # pieces per rank (1/N of the hot band around the mound + 1/N of the
+        # far field, stepped concurrently: DESIGN.md §6); SILT_PIECES=0 (or no
+        # peer memory) keeps contiguous strips, whose cut a short untimed
+        # pilot rescales by each strip's measured step time.
         full = device_initial_rows(args.workload, p, 0, p.ny, device)
         costs = row_costs(full)
         del full
         torch.cuda.empty_cache()
+        # pieces from N = 4 (tools/strip_times.py --pieces, C4: N = 2 pieces 0.88 vs
+        # strips 0.98, N = 4 0.88 vs 0.83, N = 8 0.87 vs 0.78); SILT_PIECES_MIN overrides
+        min_n = int(os.environ.get("SILT_PIECES_MIN", "4"))
+        if (world >= min_n and os.environ.get("SILT_PIECES", "1") != "0"
+                and os.environ.get("SILT_P2P", "1") != "0"):
+            layout = piece_partition(costs, world)
         partition = balanced_partition(costs, world)
-        for _ in range(2):  # two measured refinements
+        for _ in range(0 if layout else 2):  # two measured refinements
             pilot = StripRunner(p, world, rank, device=local, variant=variant,
                                 partition=partition)
             pilot.upload_device(device_initial_rows(args.workload, p, pilot.j0, pilot.nrows,
@@ -382,11 +393,16 @@ def main():
             pilot.close()
             partition = refine_partition(costs, partition, [float(x.item()) for x in times])
             torch.cuda.empty_cache()
-    runner = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
-    j0, nrows = runner.j0, runner.nrows
-    init = device_initial_rows(args.workload, p, j0, nrows, device)
-    runner.upload_device(init)
-    del init
+    if layout:
+        runner = PieceRunner(p, world, rank, layout, device=local, variant=variant)
+        runner.upload_rows(lambda a, n: device_initial_rows(args.workload, p, a, n, device))
+        j0, nrows = runner.j0, runner.nrows
+    else:
+        runner = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
+        j0, nrows = runner.j0, runner.nrows
+        init = device_initial_rows(args.workload, p, j0, nrows, device)
+        runner.upload_device(init)
+        del init
     total = args.warmup + args.steps
     runner.begin(max_steps=total + 1)
     runner.step(args.warmup)
@@ -399,8 +415,10 @@ def main():
     runner.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        runner.record_join()
         ev0.record(stream)
         runner.step(args.steps)
+        runner.record_join()
         ev1.record(stream)
         torch.cuda.synchronize()
     runner.barrier()
@@ -432,27 +450,42 @@ def main():
     # field -> device, K steps, device -> pinned host
     e2e = None
     if not args.no_e2e:
-        host = torch.empty((nrows, p.nx, 4), dtype=torch.float64, pin_memory=True)
-        host.copy_(device_initial_rows(args.workload, p, j0, nrows, device).cpu())
-        out = torch.empty_like(host, pin_memory=True)
-        runner2 = StripRunner(p, world, rank, device=local, variant=variant, partition=partition)
+        ranges = ([(q["j0"], q["n"]) for q in runner.pieces] if layout else [(j0, nrows)])
+        hosts = []
+        for a, n in ranges:
+            h = torch.empty((n, p.nx, 4), dtype=torch.float64, pin_memory=True)
+            h.copy_(device_initial_rows(args.workload, p, a, n, device).cpu())
+            hosts.append(h)
+        outs = [torch.empty_like(h, pin_memory=True) for h in hosts]
+        if layout:
+            runner2 = PieceRunner(p, world, rank, layout, device=local, variant=variant)
+        else:
+            runner2 = StripRunner(p, world, rank, device=local, variant=variant,
+                                  partition=partition)
         runner2.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        runner2.upload_host(host)
+        if layout:
+            runner2.upload_host_tensors(hosts)
+        else:
+            runner2.upload_host(hosts[0])
         runner2.begin(max_steps=args.steps)
         runner2.step(args.steps)
-        runner2.download_host(out)
+        if layout:
+            runner2.download_host_tensors(outs)
+        else:
+            runner2.download_host(outs[0])
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         runner2.barrier()
         el = runner.max_over_ranks(el)
+        nbytes = sum(h.numel() for h in hosts) * 8 * world
         e2e = {"value": cells * args.steps / el, "unit": "cell-updates/s",
-               "h2d_bytes_per_step": int(host.numel() * 8 * world / args.steps),
-               "d2h_bytes_per_step": int(out.numel() * 8 * world / args.steps),
+               "h2d_bytes_per_step": int(nbytes / args.steps),
+               "d2h_bytes_per_step": int(nbytes / args.steps),
                "timing": "wall clock around upload+begin+K steps+download, max over ranks"}
         runner2.close()
-        del host, out
+        del hosts, outs
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -484,7 +517,8 @@ def main():
             "variant": args.variant,
             "config": workload_config(args, p),
             "layout": {"rows_per_gpu": nrows, "parallelism": f"row strips x{world}",
-                       "partition": (args.partition if world > 1 else "single strip"),
+                       "partition": ("two pieces per rank: " + str(layout) if layout
+                                     else args.partition if world > 1 else "single strip"),
                        "l2": ("state 64 B/cell x %d cells >> 126 MB L2; no flush" % cells
                               if 64 * cells > 4 * 126e6 else
                               "state 64 B/cell x %d cells is L2-sized; not flushed (a step re-reads "

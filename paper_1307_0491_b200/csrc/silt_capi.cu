@@ -28,6 +28,11 @@
 #include "silt_layout.h"
 
 namespace {
+void ipc_close(void* p);          // IPC registry (multi-process strips), defined below
+void ipc_forget_local(void* p);
+}  // namespace
+
+namespace {
 
 thread_local std::string g_err;
 
@@ -643,7 +648,8 @@ int silt_solver_destroy(silt_solver* s) {
     cudaFree(s->snapbuf);
     cudaFree(s->rb_mem);
     cudaFree(s->split_map);
-    for (void* p : s->p2p_opened) cudaIpcCloseMemHandle(p);
+    for (void* p : s->p2p_opened) ipc_close(p);
+    for (void* p : {(void*)s->rows, (void*)s->ctl, (void*)s->p2p_flags}) ipc_forget_local(p);
     cudaFree(s->p2p_peer_ctl);
     cudaFree(s->p2p_peer_flag_dev);
     cudaFree(s->p2p_flags);
@@ -2029,6 +2035,80 @@ extern "C" int silt_solver_capture_write(silt_solver* s, double time, const char
 // ---- multi-process strips over peer memory ----------------------------------------
 namespace {
 
+// Process-wide registry of IPC handles.  A process may own several strips
+// ("pieces", distributed.PieceRunner) that connect to the same remote
+// buffers, and a piece's neighbour may live in the same process: handles this
+// process exported resolve to the local pointer (CUDA refuses to open them),
+// remote ones are opened once and reference-counted.
+struct IpcEntry {
+    void* ptr = nullptr;
+    int refs = 0;
+    bool local = false;
+};
+std::mutex g_ipc_mu;
+std::map<std::string, IpcEntry>& ipc_registry() {
+    static std::map<std::string, IpcEntry> m;
+    return m;
+}
+
+std::string ipc_key(const cudaIpcMemHandle_t& h) {
+    return std::string(reinterpret_cast<const char*>(&h), sizeof h);
+}
+
+int ipc_export(void* ptr, cudaIpcMemHandle_t* h) {
+    CUDA_TRY(cudaIpcGetMemHandle(h, ptr));
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    IpcEntry& e = ipc_registry()[ipc_key(*h)];
+    e.ptr = ptr;
+    e.local = true;
+    return SILT_OK;
+}
+
+int ipc_open(const cudaIpcMemHandle_t& h, void** out) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto& reg = ipc_registry();
+    auto it = reg.find(ipc_key(h));
+    if (it != reg.end() && (it->second.local || it->second.refs > 0)) {
+        if (!it->second.local) ++it->second.refs;
+        *out = it->second.ptr;
+        return SILT_OK;
+    }
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    IpcEntry& e = reg[ipc_key(h)];
+    e.ptr = p;
+    e.refs = 1;
+    e.local = false;
+    *out = p;
+    return SILT_OK;
+}
+
+void ipc_close(void* p) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto& reg = ipc_registry();
+    for (auto it = reg.begin(); it != reg.end(); ++it) {
+        if (it->second.ptr != p || it->second.local) continue;
+        if (--it->second.refs <= 0) {
+            cudaIpcCloseMemHandle(p);
+            reg.erase(it);
+        }
+        return;
+    }
+}
+
+// A local buffer about to be freed: drop its exported handle.
+void ipc_forget_local(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto& reg = ipc_registry();
+    for (auto it = reg.begin(); it != reg.end();) {
+        if (it->second.local && it->second.ptr == p)
+            it = reg.erase(it);
+        else
+            ++it;
+    }
+}
+
 // Bound of the per-step wait for the peers (SILT_P2P_TIMEOUT_MS, default 60 s).
 unsigned long long p2p_timeout_ns() {
     static const unsigned long long ns = [] {
@@ -2051,11 +2131,11 @@ extern "C" int silt_solver_p2p_export(silt_solver* s, silt_p2p_handle* out) {
     }
     std::memset(out, 0, sizeof *out);
     cudaIpcMemHandle_t h;
-    CUDA_TRY(cudaIpcGetMemHandle(&h, s->rows));
+    if (int rc = ipc_export(s->rows, &h)) return rc;
     std::memcpy(out->rows, &h, sizeof h);
-    CUDA_TRY(cudaIpcGetMemHandle(&h, s->ctl));
+    if (int rc = ipc_export(s->ctl, &h)) return rc;
     std::memcpy(out->ctl, &h, sizeof h);
-    CUDA_TRY(cudaIpcGetMemHandle(&h, s->p2p_flags));
+    if (int rc = ipc_export(s->p2p_flags, &h)) return rc;
     std::memcpy(out->flags, &h, sizeof h);
     out->nx = s->nx;
     return SILT_OK;
@@ -2076,14 +2156,14 @@ extern "C" int silt_solver_p2p_connect(silt_solver* s, int rank, int world,
         if (all[j].nx != s->nx) return fail(SILT_ERR_INVALID, "p2p: strips of different widths");
         cudaIpcMemHandle_t h;
         std::memcpy(&h, all[j].ctl, sizeof h);
-        CUDA_TRY(cudaIpcOpenMemHandle(&ctls[j], h, cudaIpcMemLazyEnablePeerAccess));
+        if (int rc = ipc_open(h, &ctls[j])) return rc;
         s->p2p_opened.push_back(ctls[j]);
         std::memcpy(&h, all[j].flags, sizeof h);
-        CUDA_TRY(cudaIpcOpenMemHandle(&flags[j], h, cudaIpcMemLazyEnablePeerAccess));
+        if (int rc = ipc_open(h, &flags[j])) return rc;
         s->p2p_opened.push_back(flags[j]);
         if (j == south || j == north) {
             std::memcpy(&h, all[j].rows, sizeof h);
-            CUDA_TRY(cudaIpcOpenMemHandle(&rows[j], h, cudaIpcMemLazyEnablePeerAccess));
+            if (int rc = ipc_open(h, &rows[j])) return rc;
             s->p2p_opened.push_back(rows[j]);
         }
     }

@@ -418,6 +418,9 @@ class StripRunner:
         if self.torch_stream is not None:
             self.torch_stream.synchronize()
 
+    def record_join(self):
+        """(PieceRunner interface) the solver's stream IS torch_stream."""
+
     def barrier(self):
         if self._dist is not None:
             self._dist.barrier()
@@ -548,3 +551,241 @@ class LocalStripGroup:
         if self.h:
             self.L.silt_group_destroy(self.h)
             self.h = None
+
+
+# ---- two pieces per rank ------------------------------------------------------
+# A contiguous strip through the mound is all full-path work: its GPU has no
+# quiescent rows for the hot CTAs to overlap with, so on C4 the strips bound
+# strong scaling at ~0.77 (N = 8, profiles/r1_strip_balance.md).  Here every
+# rank owns TWO row ranges: 1/N of the hot band around the mound and 1/N of the
+# far field, stepped as two solvers on two streams of its GPU, so hot and
+# quiescent CTAs share the GPU as in the one-GPU launch (tools/strip_times.py
+# --pieces: 0.86 at N = 8).  Any layout gives bit-identical fields (the
+# reference's layout contract, tests/test_parallel.cpp:215-238).
+
+
+def piece_partition(row_cost, world: int, spread: int | None = None):
+    """Two row ranges per rank: [(hot j0, n), (far j0, n)] for ranks 0..world-1.
+
+    Hot band = the rows of non-quiescent work (row_cost above the quiescent
+    level) widened by `spread` rows on both sides (default 2 % of the rows:
+    the waves a run sends out), split at equal modelled cost.  The far field
+    (the rows below and above the band) is split into `world` pieces of equal
+    rows; the pieces BELOW the band go to ranks world//2 .. world-1 and those
+    ABOVE to ranks 0 .. world//2 - 1, so no two pieces of one rank are row
+    neighbours.  Returns None when the grid has no distinct hot band (then
+    contiguous strips are the better layout)."""
+    cost = np.asarray(row_cost, dtype=np.float64)
+    ny = cost.size
+    if world < 2 or ny < 4 * world:
+        return None
+    quiet = cost.min()
+    hot_rows = np.nonzero(cost > quiet * (1 + 1e-9))[0]
+    if hot_rows.size == 0:
+        return None
+    spread = max(1, int(0.02 * ny)) if spread is None else spread
+    lo = max(0, int(hot_rows[0]) - spread)
+    hi = min(ny, int(hot_rows[-1]) + 1 + spread)
+    half = world // 2
+    n_lo_pieces, n_hi_pieces = world - half, half
+    if hi - lo < world or lo < n_lo_pieces or ny - hi < n_hi_pieces or n_hi_pieces == 0:
+        return None
+    hot = [(lo + j0, n) for j0, n in balanced_partition(cost[lo:hi], world)]
+    out = []
+    for r in range(world):
+        if r >= half:  # far piece below the band
+            j0, n = block_range(lo, n_lo_pieces, r - half)
+        else:          # far piece above the band
+            j0, n = block_range(ny - hi, n_hi_pieces, r)
+            j0 += hi
+        out.append([hot[r], (j0, n)])
+    return out
+
+
+def piece_order(layout):
+    """All pieces in row order: [(j0, n, rank, k)] (k = 0 hot, 1 far)."""
+    pieces = [(j0, n, r, k) for r, ps in enumerate(layout) for k, (j0, n) in enumerate(ps)]
+    return sorted(pieces)
+
+
+class PieceRunner:
+    """One rank's pieces (see piece_partition): a CUDA solver per piece on its
+    own stream, exchanging over peer memory with every piece of every rank
+    ("virtual ranks" = pieces in row order).  Per step, with no host
+    synchronisation: each piece's step kernel stores its edge rows into the
+    neighbouring pieces' receive rows and its axis-speed maxima into every
+    piece's slot, and waits (bounded) for every piece's previous step before
+    it starts — exactly the StripRunner peer-memory protocol, with 2N
+    participants.  Requires peer memory (CUDA IPC); 2D, non-periodic y."""
+
+    def __init__(self, problem, world: int, rank: int, layout, device: int = 0,
+                 variant: int = abi.VARIANT_FAST):
+        import torch
+        import torch.distributed as dist
+        from . import native
+        if problem.dim != 2 or problem.bc[abi.SOUTH].type == abi.BC_PERIODIC:
+            raise ValueError("pieces: 2D grids with non-periodic y only")
+        self.problem, self.world, self.rank = problem, world, rank
+        self.layout = layout
+        self._dist = dist
+        self.device = torch.device("cuda", device)
+        order = piece_order(layout)
+        self.vworld = len(order)
+        vid = {(r, k): v for v, (_, _, r, k) in enumerate(order)}
+        self.pieces = []
+        # the hot piece runs 32-row blocks (tools/strip_times.py --pieces: 32
+        # beat the launch-size default, 8 and 16 on C4 at N = 4 and 8);
+        # SILT_ROWS set by the caller wins
+        hot_rows = os.environ.get("SILT_PIECE_HOT_ROWS", "32")
+        for k, (j0, n) in enumerate(layout[rank]):
+            v = vid[(rank, k)]
+            south = v - 1 if v > 0 else None
+            north = v + 1 if v < self.vworld - 1 else None
+            strip = abi.SiltStrip(j0, n, int(south is not None), int(north is not None))
+            user_rows = os.environ.get("SILT_ROWS")
+            if k == 0 and user_rows is None and hot_rows != "0":
+                os.environ["SILT_ROWS"] = hot_rows
+            try:
+                s = native.Solver(problem, strip, device, variant)
+            finally:
+                if user_rows is None:
+                    os.environ.pop("SILT_ROWS", None)
+            st = torch.cuda.Stream(device=device)
+            s.set_stream(st.cuda_stream)
+            self.pieces.append({"j0": j0, "n": n, "v": v, "south": south, "north": north,
+                                "solver": s, "stream": st})
+        # handshake: every piece's handles, in virtual-rank order
+        mine = [(p["v"], p["solver"].p2p_export()) for p in self.pieces]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        handles = [None] * self.vworld
+        for lst in allh:
+            for v, h in lst:
+                handles[v] = h
+        ok = 1
+        try:
+            for p in self.pieces:
+                p["solver"].p2p_connect(p["v"], self.vworld, handles, p["south"], p["north"])
+        except Exception:
+            ok = 0
+        t = torch.tensor([ok], dtype=torch.int32, device=self._reduce_device())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) != 1:
+            raise RuntimeError("pieces: peer-memory connection failed on some rank")
+        self.torch_stream = torch.cuda.Stream(device=device)  # joins the pieces' streams
+        self.j0 = min(p["j0"] for p in self.pieces)
+        self.nrows = sum(p["n"] for p in self.pieces)
+        self._p2p = True
+
+    def _reduce_device(self):
+        return "cpu" if self._dist.get_backend() == "gloo" else self.device
+
+    # ---- run control ------------------------------------------------------
+    def upload_rows(self, rows_fn):
+        """rows_fn(j0, n) -> device tensor (n, nx, 4) of the piece's initial rows."""
+        import torch
+        for p in self.pieces:
+            t = rows_fn(p["j0"], p["n"])
+            torch.cuda.current_stream(self.device).synchronize()
+            p["solver"].upload_device(t.data_ptr())
+            p["stream"].synchronize()
+
+    def upload_host(self, full):
+        """Rows of the WHOLE grid (host array); each piece takes its own."""
+        for p in self.pieces:
+            p["solver"].upload(np.ascontiguousarray(full[p["j0"]:p["j0"] + p["n"]]))
+
+    def upload_host_tensors(self, tensors):
+        """One (n, nx, 4) host tensor per piece (pinned: the copy is async)."""
+        from .native import check
+        for p, t in zip(self.pieces, tensors):
+            s = p["solver"]
+            check(s.L.silt_solver_upload(s.h, C.cast(t.data_ptr(), C.POINTER(C.c_double))))
+
+    def download_host_tensors(self, tensors):
+        from .native import check
+        for p, t in zip(self.pieces, tensors):
+            s = p["solver"]
+            check(s.L.silt_solver_download(s.h, C.cast(t.data_ptr(), C.POINTER(C.c_double))))
+
+    def begin(self, t_end: float = np.inf, max_steps: int = -1, snapshots=(), dt_cap: int = 0):
+        import torch
+        if snapshots:
+            raise ValueError("pieces: snapshots are not supported (use StripRunner)")
+        for p in self.pieces:
+            p["solver"].begin(t_end=t_end, max_steps=max_steps, dt_cap=dt_cap)
+        # global MAX of the initial axis speeds over every piece (global_dt,
+        # src/parallel.cpp:200-206); the initial reduction kernels delivered
+        # the edge rows themselves
+        slots = [torch.as_tensor(_CAI(p["solver"].reduce_slot(), 2), device=self.device)
+                 for p in self.pieces]
+        for p in self.pieces:
+            p["stream"].synchronize()
+        m = torch.stack(slots).max(dim=0).values
+        dev = self._reduce_device()
+        m = m.to(dev)
+        self._dist.all_reduce(m, op=self._dist.ReduceOp.MAX)
+        m = m.to(self.device)
+        for s in slots:
+            s.copy_(m)
+        torch.cuda.synchronize(self.device)
+
+    def step(self, n: int = 1):
+        for _ in range(n):
+            for p in self.pieces:
+                p["solver"].p2p_step(1)
+
+    def record_join(self):
+        """Make torch_stream wait for every piece's stream (for events)."""
+        for p in self.pieces:
+            self.torch_stream.wait_stream(p["stream"])
+
+    def synchronize(self):
+        for p in self.pieces:
+            p["stream"].synchronize()
+
+    def status(self):
+        sts = [p["solver"].status() for p in self.pieces]
+        return sts[0]
+
+    def launch_count(self) -> int:
+        return sum(p["solver"].launch_count() for p in self.pieces)
+
+    def barrier(self):
+        self._dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self._reduce_device())
+        self._dist.all_reduce(t, op=self._dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def dt_log(self, n: int):
+        return self.pieces[0]["solver"].dt_log(n)
+
+    def gather(self):
+        """The global field on rank 0 (every piece's rows at its offset)."""
+        mine = [(p["j0"], p["solver"].download()) for p in self.pieces]
+        parts = [None] * self.world if self.rank == 0 else None
+        self._dist.gather_object(mine, parts, dst=0)
+        if self.rank != 0:
+            return None
+        ny, nx = self.problem.ny, self.problem.nx
+        out = np.empty((ny, nx, 4))
+        for lst in parts:
+            for j0, a in lst:
+                out[j0:j0 + a.shape[0]] = a
+        return out
+
+    def close(self):
+        # peers may still be storing into this rank's memory: drain, then
+        # every rank frees together
+        self.synchronize()
+        self._dist.barrier()
+        for p in self.pieces:
+            p["solver"].close()
+        self.pieces = []
+
+    def shutdown(self):
+        if self._dist.is_initialized():
+            self._dist.destroy_process_group()

@@ -131,3 +131,28 @@ def test_balanced_partition_properties():
         if n > 1000:
             loads = [cost[o:o + c].sum() for o, c in part]
             assert max(loads) <= 1.01 * sum(loads) / parts
+
+
+def test_piece_partition_layout():
+    """Two pieces per rank (distributed.piece_partition): the 2N pieces tile
+    the rows exactly once, the hot pieces cover the mound's rows, and no two
+    pieces of one rank are row neighbours (their exchange is always between
+    processes)."""
+    from paper_1307_0491_b200 import scenarios
+    from paper_1307_0491_b200.distributed import piece_order, piece_partition, row_costs
+    p, init, _ = scenarios.dune_2d(1024)
+    costs = row_costs(init)
+    hot_rows = np.nonzero(costs > costs.min() * (1 + 1e-9))[0]
+    for world in (2, 3, 4, 5, 8):
+        layout = piece_partition(costs, world)
+        assert len(layout) == world and all(len(x) == 2 for x in layout)
+        order = piece_order(layout)
+        assert order[0][0] == 0 and sum(n for _, n, _, _ in order) == 1024
+        assert all(a[0] + a[1] == b[0] for a, b in zip(order, order[1:]))
+        assert all(a[2] != b[2] for a, b in zip(order, order[1:]))
+        hot = [x[0] for x in layout]
+        lo, hi = min(j for j, _ in hot), max(j + n for j, n in hot)
+        assert lo <= hot_rows[0] and hi > hot_rows[-1]
+    # a grid without a distinct hot band keeps contiguous strips
+    flat = np.ones(1024)
+    assert piece_partition(flat, 4) is None

@@ -89,6 +89,63 @@ def test_strip_runner_ranks_on_one_gpu(tmp_path, golden, world, case):
             assert np.all(normwise(field, data[f"{case}_final"]) <= 1e-9)
 
 
+def _piece_worker(rank, world, port, n, steps, out_dir, variant):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0")
+    sys.path.insert(0, ROOT)
+    import torch
+    from paper_1307_0491_b200 import scenarios
+    from paper_1307_0491_b200.distributed import PieceRunner, init_dist, piece_partition, row_costs
+    p, init, _ = scenarios.dune_2d(n)
+    torch.cuda.set_device(0)
+    init_dist(world, backend="gloo")
+    layout = piece_partition(row_costs(init), world)
+    runner = PieceRunner(p, world, rank, layout, device=0, variant=variant)
+    runner.upload_host(init)
+    runner.begin(max_steps=steps, dt_cap=steps)
+    runner.step(steps)
+    runner.synchronize()
+    st = runner.status()
+    field = runner.gather()
+    if rank == 0:
+        np.save(os.path.join(out_dir, "field.npy"), field)
+        np.save(os.path.join(out_dir, "meta.npy"), np.array([st.t, st.steps]))
+        np.save(os.path.join(out_dir, "dt.npy"), runner.dt_log(steps))
+        with open(os.path.join(out_dir, "layout.txt"), "w") as fh:
+            fh.write(repr(layout))
+    runner.close()
+    runner.shutdown()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_two_pieces_per_rank_on_one_gpu(tmp_path, restatement, world):
+    """PieceRunner (two row ranges per rank — 1/N of the hot band around the
+    mound + 1/N of the far field — stepped concurrently, peer-memory exchange
+    between all 2N pieces): bitwise equal to the reference's serial run
+    (STRICT), FAST within the bar."""
+    import torch.multiprocessing as mp
+    from paper_1307_0491_b200 import abi, scenarios
+    if os.environ.get("SILT_P2P", "1") == "0":
+        pytest.skip("peer-memory path disabled")
+    n, steps = 160, 30
+    p, init, _ = scenarios.dune_2d(n)
+    ref, t, sn, log = restatement.run(p, init, max_steps=steps)
+    for variant in (abi.VARIANT_STRICT, abi.VARIANT_FAST):
+        out = tmp_path / f"v{variant}"
+        out.mkdir()
+        mp.spawn(_piece_worker, args=(world, _free_port(), n, steps, str(out), variant),
+                 nprocs=world, join=True)
+        field = np.load(out / "field.npy")
+        t_got, steps_got = np.load(out / "meta.npy")
+        assert steps_got == sn
+        if variant == abi.VARIANT_STRICT:
+            assert t_got == t
+            assert np.array_equal(np.load(out / "dt.npy"), log)
+            assert np.array_equal(field, ref), (out / "layout.txt").read_text()
+        else:
+            assert np.all(normwise(field, ref) <= 1e-9)
+
+
 def _hung_peer_worker(rank, world, port, case, out_dir):
     """Rank 1 stops stepping after begin (a hung or dying peer); rank 0's
     bounded peer wait must turn that into an error instead of spinning."""
@@ -159,12 +216,12 @@ def test_uneven_partition_on_one_gpu(tmp_path, golden):
 
 
 def test_bench_two_ranks_on_one_gpu():
-    """bench.py's N > 1 path (torchrun, balanced strips with the measured
-    pilot refinement, max-over-ranks timing, e2e) end to end, two ranks
-    sharing the GPU over gloo: one valid JSON line from rank 0."""
+    """bench.py's N > 1 path (torchrun, the two-pieces-per-rank layout forced
+    down to N = 2, max-over-ranks timing, e2e) end to end, two ranks sharing
+    the GPU over gloo: one valid JSON line from rank 0."""
     import json
     import subprocess
-    env = dict(os.environ, SILT_DIST_BACKEND="gloo")
+    env = dict(os.environ, SILT_DIST_BACKEND="gloo", SILT_PIECES_MIN="2")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "C3", "--steps", "3",
@@ -176,4 +233,5 @@ def test_bench_two_ranks_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
     assert d["layout"]["parallelism"] == "row strips x2"
+    assert d["layout"]["partition"].startswith("two pieces per rank")
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0

@@ -18,6 +18,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 import torch  # noqa: E402
 
@@ -59,6 +60,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ns", default="2,4,8", help="strip counts to measure")
+    ap.add_argument("--pieces", action="store_true",
+                    help="also the two-pieces-per-rank layout (distributed.piece_partition)")
     a = ap.parse_args()
     p = bench.build_global_problem(a.workload, 1)
     full = bench.device_initial_rows(a.workload, p, 0, p.ny, torch.device("cuda"))
@@ -78,6 +81,18 @@ def main():
             out["runs"].append({"n": n, "partition": name, "rows": [c for _, c in part],
                                 "strip_ms": ts, "max_ms": max(ts), "efficiency": eff})
             print(f"N={n} {name:8s} max {max(ts):.3f} ms  eff {eff:.2f}  strips "
+                  + " ".join(f"{x:.2f}" for x in ts), flush=True)
+        if a.pieces:
+            from two_piece_probe import rank_ms
+            from paper_1307_0491_b200.distributed import piece_partition
+            layout = piece_partition(costs, n)
+            hr = int(os.environ.get("SILT_PIECE_HOT_ROWS", "32"))
+            ts = [rank_ms(p, full, [(h0, hn, hr), (f0, fn, 0)], a.steps, a.warmup)
+                  for (h0, hn), (f0, fn) in layout]
+            eff = t1 / (n * max(ts))
+            out["runs"].append({"n": n, "partition": "pieces", "layout": layout, "rank_ms": ts,
+                                "max_ms": max(ts), "efficiency": eff})
+            print(f"N={n} pieces   max {max(ts):.3f} ms  eff {eff:.2f}  ranks "
                   + " ".join(f"{x:.2f}" for x in ts), flush=True)
     print(json.dumps(out))
 
