@@ -151,17 +151,20 @@ def main():
             if mix:
                 tot = sum(v for _, v in mix)
                 fp64 = sum(v for op, v in mix if op in ("DFMA", "DMUL", "DADD", "DSETP"))
+                k = "smsp__thread_inst_executed_per_inst_executed.ratio"
+                lanes = float(res[k][1]) if k in res else 32.0
                 fh.write("\nDynamic instruction mix (executed warp instructions per SASS opcode, "
                          "`sass__inst_executed_per_opcode`)")
                 if a.cells:
-                    fh.write(f"; per cell-update = count / {int(a.cells)} x 32 lanes")
+                    fh.write(f"; per cell-update = count x {lanes:.2f} active lanes per warp "
+                             f"instruction / {int(a.cells)} cells (thread instructions)")
                 fh.write(f".  FP64 pipe (DFMA+DMUL+DADD+DSETP): {100 * fp64 / tot:.1f}% of "
                          "all instructions.\n\n| opcode | warp instructions | share |"
                          + (" per cell-update |" if a.cells else "") + "\n|---|---|---|"
                          + ("---|" if a.cells else "") + "\n")
                 for op, v in mix[:24]:
                     fh.write(f"| {op} | {v} | {100 * v / tot:.1f}% |"
-                             + (f" {32 * v / a.cells:.1f} |" if a.cells else "") + "\n")
+                             + (f" {lanes * v / a.cells:.1f} |" if a.cells else "") + "\n")
 
 
 if __name__ == "__main__":
