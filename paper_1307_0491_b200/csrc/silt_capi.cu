@@ -592,7 +592,30 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         A.rb_order = order ? 1 : 0;
         A.epilogue = 1;
         A.rb_map = nullptr;
-        if (!order && problem->dim == 2 && nb >= 3 && (st.south_neighbor || st.north_neighbor)) {
+        // Warp-item mode for short 2D launches (a few waves of CTAs, e.g. C3):
+        // one wave of resident CTAs whose warps pull (band, row block) items
+        // from a counter.  Not with the split edge/interior launches of the
+        // collective multi-rank path.  SILT_WARP_ITEMS=0/1 forces it off/on.
+        A.warp_items = 0;
+        A.bands = (int)strips;
+        A.n_items = (int)(strips * nb);
+        A.warps_total = 0;
+        {
+            const double waves = (double)ctas / ((double)ctas_per_sm * sms);
+            const char* we = std::getenv("SILT_WARP_ITEMS");
+            const bool neighbours = st.south_neighbor || st.north_neighbor;
+            bool wi = problem->dim == 2 && !order && !neighbours && waves <= 8.0 && waves > 1.0;
+            if (we) wi = problem->dim == 2 && !order && we[0] == '1';
+            if (wi) {
+                const unsigned grid = (unsigned)std::min<long long>(
+                    ctas, (long long)ctas_per_sm * sms);
+                s->step_grid = dim3(grid, 1, 1);
+                A.warp_items = 1;
+                A.warps_total = (int)grid * warps_per_cta;
+            }
+        }
+        if (!A.warp_items && !order && problem->dim == 2 && nb >= 3 &&
+            (st.south_neighbor || st.north_neighbor)) {
             std::vector<int> m{0, (int)nb - 1};
             for (unsigned k = 1; k + 1 < nb; ++k) m.push_back((int)k);
             if (cudaMalloc(&s->split_map, m.size() * sizeof(int)) != cudaSuccess)

@@ -127,6 +127,7 @@ __device__ __forceinline__ void control_epilogue(const StepArgs& A, int li, cons
     clr.max_sx = clr.max_sy = clr.hmax = 0ull;
     clr.wet = 0u;
     clr.err = 0u;
+    C.item_ctr[(li + 2) % 3] = 0u;  // warp-item counter of launch li + 2
     if (d.run) {
         nxt.t = d.t_new;
         nxt.steps = cur.steps + 1;
@@ -553,7 +554,7 @@ struct StepSmem {
 // row block counts as hot for the next launch's order.
 constexpr int kHotRows = 4;
 
-template <bool S, bool SH>
+template <bool S, bool SH, bool WI = false>
 __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_kernel(StepArgs A, int li) {
     // Per-thread march state in shared memory (SoA by thread: conflict-free),
     // so that registers at each face solve hold little beyond the solver.
@@ -575,26 +576,43 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     const int p = (int)(cur.steps & 1), q = p ^ 1;
     const int t = threadIdx.x;
     const int lane = t & 31;
-    const int strip = blockIdx.x * (kStepThreads / 32) + (t >> 5);
+    const double cx = d.dt / A.dx;
+    const double cy = d.dt / A.dy;
+    const double href = __longlong_as_double((long long)cur.hmax);
+    Reduce R{0.0, 0.0, 0.0, 0u};
+    // Work items.  Default: one (column band, row block) per warp, from the
+    // launch grid.  Warp-item mode (WI: short launches, A.warp_items): the grid
+    // is one wave of resident CTAs and every warp pulls (band, row block)
+    // items from a per-launch counter until none are left — no partly empty
+    // last wave and no CTA start-up per item; the maxima of all the warp's
+    // items fold into one reduction.
+    const int gwarp = (blockIdx.x + blockIdx.y * gridDim.x) * (kStepThreads / 32) + (t >> 5);
+    int item = gwarp;
+    do {
+    {
+    int strip, rbi;
+    if constexpr (WI) {
+        strip = item % A.bands;
+        rbi = item / A.bands;
+    } else {
+        strip = blockIdx.x * (kStepThreads / 32) + (t >> 5);
+        rbi = A.rb_map ? __ldg(A.rb_map + blockIdx.y) : (int)blockIdx.y;
+    }
     const int i0 = strip * kCellsPerWarp;
-    if (i0 >= A.nx) return;  // warp-uniform
+    if (i0 >= A.nx) goto item_done;  // warp-uniform
     const int col = i0 - 1 + lane;
     const bool owned = lane >= 1 && lane <= kCellsPerWarp && col < A.nx;
     const bool xface = lane <= kCellsPerWarp && col <= A.nx - 1;  // face at right of col
-    const int jb = (A.rb_map ? __ldg(A.rb_map + blockIdx.y) : (int)blockIdx.y) * A.rows_per_block;
+    const int jb = rbi * A.rows_per_block;
     const int je = min(jb + A.rows_per_block, A.ny);
-    if (jb >= je) return;
+    if (jb >= je) goto item_done;
     if (lane == 0) sm.nfull[t >> 5] = 0;
 #ifdef SILT_TRACE
     unsigned long long tr_start = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
 #endif
-    const double cx = d.dt / A.dx;
-    const double cy = d.dt / A.dy;
-    const double href = __longlong_as_double((long long)cur.hmax);
     const RowSrc src = row_src(A, p, col);
 
-    Reduce R{0.0, 0.0, 0.0, 0u};
     const unsigned row_sa0 = (unsigned)__cvta_generic_to_shared(&sh_row[0][0][t]);
     constexpr unsigned kSlotBytes = 4 * kStepThreads * sizeof(double);
     double* const out0 = A.state[q][0] + col;  // output cell (row 0) of field 0
@@ -650,7 +668,7 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         buf = buf == SILT_RING - 1 ? 0 : buf + 1;
         if (SILT_VIOLATED(blockDim.x == kStepThreads && buf >= 0 && buf < SILT_RING, 4, buf,
                           blockDim.x))
-            return;
+            goto item_done;
         fix_xghost(A, col, r, c);
         const bool own_row = r >= jb && r < je;
 
@@ -801,13 +819,11 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
         sh_xs[3][t] = c[3] - cx * (fx.z - lz);
         __syncwarp();
     }
-    if (A.rb_order && lane == 0 && sm.nfull[t >> 5] > kHotRows)
-        A.rb_hot[li][__ldg(A.rb_map + blockIdx.y)] = 1;
-    reduce_flush(R, nxt);
+    if (A.rb_order && lane == 0 && sm.nfull[t >> 5] > kHotRows) A.rb_hot[li][rbi] = 1;
 #ifdef SILT_TRACE
-    // (trace build only) per-warp fold into the CTA's record; the buffer is
-    // initialised to {~0, 0, 0, 0} by the tool
-    if (!S && g_trace && lane == 0) {
+    // (trace build only, launch-grid mode) per-warp fold into the CTA's
+    // record; the buffer is initialised to {~0, 0, 0, 0} by the tool
+    if (!S && !WI && g_trace && lane == 0) {
         unsigned long long tr_end;
         unsigned smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_end));
@@ -820,6 +836,16 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
                                 ((unsigned long long)sm.nfull[t >> 5] << 32));
     }
 #endif
+    }
+    item_done:
+        if constexpr (!WI) break;
+        {
+            unsigned nxt_item = 0;
+            if (lane == 0) nxt_item = atomicAdd(&A.ctl->item_ctr[li % 3], 1u);
+            item = A.warps_total + (int)__shfl_sync(0xffffffffu, nxt_item, 0);
+        }
+    } while (item < A.n_items);
+    reduce_flush(R, nxt);
 }
 
 // ---- K2: 1D step (step_1d, src/stepper.cpp:118-140) ----------------------
@@ -1242,18 +1268,25 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
             int dev_ = 0;                                                                        \
             cudaGetDevice(&dev_);                                                                \
             if (!(attr_set >> (dev_ & 63) & 1ull)) {                                             \
-                cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH>,                             \
+                cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH, false>,                      \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                                     (int)sizeof(silt_dev::StepSmem));                           \
+                cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH, true>,                       \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,                \
                                      (int)sizeof(silt_dev::StepSmem));                           \
                 /* SILT_CARVEOUT=%: shared-memory carveout preference (A/B) */                  \
                 if (const char* cv = std::getenv("SILT_CARVEOUT"))                               \
-                    cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH>,                         \
+                    cudaFuncSetAttribute(silt_dev::step2d_kernel<S, SH, false>,                  \
                                          cudaFuncAttributePreferredSharedMemoryCarveout,         \
                                          std::atoi(cv));                                         \
                 attr_set |= 1ull << (dev_ & 63);                                                 \
             }                                                                                    \
-            silt_dev::step2d_kernel<S, SH>                                                       \
-                <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);                 \
+            if (A.warp_items)                                                                    \
+                silt_dev::step2d_kernel<S, SH, true>                                             \
+                    <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);             \
+            else                                                                                 \
+                silt_dev::step2d_kernel<S, SH, false>                                            \
+                    <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);             \
         } else                                                                                   \
             silt_dev::step1d_kernel<S, SH><<<grid, kStepThreads, 0, st>>>(A, li);                \
     }                                                                                            \

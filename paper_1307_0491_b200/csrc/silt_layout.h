@@ -52,6 +52,7 @@ struct Control {
     unsigned int err_claim;
     unsigned int err_bits;
     int err_col, err_row;
+    unsigned int item_ctr[3];  // warp-item mode: items taken per launch index (mod 3)
     int fixed_mode;       // 1: step_1d/step_2d with the caller's dt, applied as
                           // given (0, negative or NaN included), like the reference
     double err_info[6];
@@ -64,6 +65,9 @@ struct StepArgs {
     int south_nbr, north_nbr, per_y_self;
     int write_edges_in_reduce;
     int quiet_skip;         // FAST: skip provably unchanged quiescent rows
+    // Warp-item mode of the 2D step (short launches): the grid is one wave of
+    // CTAs and warps pull (band, row block) items from Control::item_ctr.
+    int warp_items, bands, n_items, warps_total;
     long long plane;        // doubles between the field planes of one parity
     // Row-block launch order (2D, long launches): launch li processes row
     // block rb_table[li][blockIdx.y]; rows with full-path (non-quiescent)

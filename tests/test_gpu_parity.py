@@ -522,11 +522,15 @@ def test_quiet_row_skip_is_bit_identical(N, golden, case, monkeypatch):
     assert np.array_equal(outs[0][0], outs[1][0])
 
 
+@pytest.mark.parametrize("items", ["0", "1"])
 @pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (2, 2), (29, 3), (30, 2), (31, 2),
-                                   (61, 5), (90, 1), (121, 9)])
-def test_degenerate_shapes(N, restatement, shape):
+                                   (61, 5), (90, 1), (121, 9), (257, 131)])
+def test_degenerate_shapes(N, restatement, shape, items, monkeypatch):
     """Grids at and around the warp band width (30 owned columns) and single
-    rows / columns, with every BC type: STRICT bitwise, FAST within the bar."""
+    rows / columns, with every BC type: STRICT bitwise, FAST within the bar;
+    with the launch grid (SILT_WARP_ITEMS=0) and with warps pulling
+    (band, row block) items from the per-launch counter (=1)."""
+    monkeypatch.setenv("SILT_WARP_ITEMS", items)
     nx, ny = shape
     rng = np.random.default_rng(nx * 131 + ny)
     init = np.empty((ny, nx, 4))
