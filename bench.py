@@ -394,7 +394,11 @@ def main():
             partition = refine_partition(costs, partition, [float(x.item()) for x in times])
             torch.cuda.empty_cache()
     if layout:
-        runner = PieceRunner(p, world, rank, layout, device=local, variant=variant)
+        try:
+            runner = PieceRunner(p, world, rank, layout, device=local, variant=variant)
+        except RuntimeError:  # no peer memory between the ranks: contiguous strips (NCCL)
+            layout = None
+    if layout:
         runner.upload_rows(lambda a, n: device_initial_rows(args.workload, p, a, n, device))
         j0, nrows = runner.j0, runner.nrows
     else:

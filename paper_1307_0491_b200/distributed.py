@@ -671,6 +671,9 @@ class PieceRunner:
         t = torch.tensor([ok], dtype=torch.int32, device=self._reduce_device())
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         if int(t.item()) != 1:
+            for p in self.pieces:
+                p["solver"].close()
+            self.pieces = []
             raise RuntimeError("pieces: peer-memory connection failed on some rank")
         self.torch_stream = torch.cuda.Stream(device=device)  # joins the pieces' streams
         self.j0 = min(p["j0"] for p in self.pieces)
