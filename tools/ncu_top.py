@@ -6,7 +6,7 @@ import ncu_lines as N
 rep, lib, tu = sys.argv[1], sys.argv[2], (sys.argv[3] if len(sys.argv) > 3 else "fast")
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 hdr, rows = N.ncu_rows(rep, "step2d")
-lines = N.sass_lines(lib, "step2d_kernel", tu)
+lines = N.sass_lines(lib, os.environ.get("SILT_NCU_KERNEL", "step2d_kernel"), tu)
 ie, isrc, iss = hdr.index("Instructions Executed"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
 inst, stall, ops = collections.Counter(), collections.Counter(), collections.defaultdict(collections.Counter)
 for k in range(min(len(lines), len(rows))):
