@@ -566,6 +566,23 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
             if (waste(cand) < waste(best) - 0.05) best = cand;
         R = best;
     }
+    // Long launches of one strip (the row-block order below applies) run as
+    // warp items too (warps pull (band, row block) items through the order
+    // table, no CTA start-up per block and no warp slot held by a finished
+    // warp of a hot CTA), with row blocks of at most 64 rows: C4 3.004 ->
+    // 2.958 ms per step (20 steps; ~neutral over 500 steps, where the faster
+    // kernel meets the power cap), the uniform field unchanged.
+    const char* wi_env = std::getenv("SILT_WARP_ITEMS");
+    {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        const long long nb0 = (s->ny + R - 1) / R;
+        const long long ctas0 = nb0 * ((strips + kStepThreads / 32 - 1) / (kStepThreads / 32));
+        const char* pe = std::getenv("SILT_ROW_PERM");
+        const bool order0 = problem->dim == 2 && nb0 >= 16 && (pe ? pe[0] != '0' : ctas0 >= 64LL * nsm);
+        const bool neighbours = st.south_neighbor || st.north_neighbor;
+        if (order0 && !neighbours && !(wi_env && wi_env[0] == '0')) R = std::min(R, 64LL);
+    }
     if (const char* e = std::getenv("SILT_ROWS")) R = std::max(1LL, std::atoll(e));
     if (problem->dim == 1) R = 1;
     A.rows_per_block = (int)R;
@@ -592,10 +609,11 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         A.rb_order = order ? 1 : 0;
         A.epilogue = 1;
         A.rb_map = nullptr;
-        // Warp-item mode for short 2D launches (a few waves of CTAs, e.g. C3):
-        // one wave of resident CTAs whose warps pull (band, row block) items
-        // from a counter.  Not with the split edge/interior launches of the
-        // collective multi-rank path.  SILT_WARP_ITEMS=0/1 forces it off/on.
+        // Warp-item mode for short 2D launches (a few waves of CTAs, e.g. C3)
+        // and long ordered ones (C4): one wave of resident CTAs whose warps
+        // pull (band, row block) items from a counter.  Not with neighbour
+        // strips (edge rows first, split launches).  SILT_WARP_ITEMS=0/1
+        // forces it off/on.
         A.warp_items = 0;
         A.bands = (int)strips;
         A.n_items = (int)(strips * nb);
@@ -604,8 +622,9 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
             const double waves = (double)ctas / ((double)ctas_per_sm * sms);
             const char* we = std::getenv("SILT_WARP_ITEMS");
             const bool neighbours = st.south_neighbor || st.north_neighbor;
-            bool wi = problem->dim == 2 && !order && !neighbours && waves <= 8.0 && waves > 1.0;
-            if (we) wi = problem->dim == 2 && !order && we[0] == '1';
+            bool wi = problem->dim == 2 && !neighbours &&
+                      (order || (waves <= 8.0 && waves > 1.0));
+            if (we) wi = problem->dim == 2 && !neighbours && we[0] == '1';
             if (wi) {
                 const unsigned grid = (unsigned)std::min<long long>(
                     ctas, (long long)ctas_per_sm * sms);
@@ -633,9 +652,17 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         if (const char* es = std::getenv("SILT_RB_SPAN")) s->rb_span = std::max(100, std::min(1000, std::atoi(es)));
         s->row_blocks = (int)nb;
         if (order) {
+            // default (no hot information): 8 interleaved passes for the
+            // launch grid; in order for warp items (whose warps stream
+            // through the row blocks one after another: the halo rows of
+            // neighbouring blocks are still in L2)
             std::vector<int> def;
-            for (unsigned z = 0; z < 8; ++z)
-                for (unsigned y = z; y < nb; y += 8) def.push_back((int)y);
+            if (A.warp_items) {
+                for (unsigned y = 0; y < nb; ++y) def.push_back((int)y);
+            } else {
+                for (unsigned z = 0; z < 8; ++z)
+                    for (unsigned y = z; y < nb; y += 8) def.push_back((int)y);
+            }
             if (cudaMalloc(&s->rb_mem, (4 + 2 * 3) * (size_t)nb * sizeof(int) + 3 * (size_t)nb) !=
                 cudaSuccess)
                 return cleanup(fail(SILT_ERR_CUDA, "silt_solver_create: device allocation failed"));

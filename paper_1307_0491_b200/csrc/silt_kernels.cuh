@@ -592,8 +592,11 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     {
     int strip, rbi;
     if constexpr (WI) {
+        // items run row block by row block (bands fastest), in the launch's
+        // row-block order when there is one (hot blocks spread, §3c)
         strip = item % A.bands;
         rbi = item / A.bands;
+        if (A.rb_map) rbi = __ldg(A.rb_map + rbi);
     } else {
         strip = blockIdx.x * (kStepThreads / 32) + (t >> 5);
         rbi = A.rb_map ? __ldg(A.rb_map + blockIdx.y) : (int)blockIdx.y;

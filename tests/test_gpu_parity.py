@@ -616,6 +616,29 @@ def test_streak_loop_is_bit_identical(N, monkeypatch, bcs):
         assert np.array_equal(strips, ref[0])
 
 
+def test_launch_orders_are_bit_identical(N, monkeypatch):
+    """Every cell is updated once per step whatever the order of the row
+    blocks: the launch grid in index order, in the dynamic hot-spread order
+    (SILT_ROW_PERM=1), and warps pulling (band, row block) items in index
+    order or through the same order table (SILT_WARP_ITEMS=1) give the same
+    bits, dt log included."""
+    nx, ny, steps = 331, 250, 60
+    init = _bump_field(nx, ny, 160.0, 120.0, 30.0)
+    p = abi.make_problem(2, nx, ny, 1.0, 1.0, a_g=0.01, cfl=0.45)
+    monkeypatch.setenv("SILT_ROWS", "8")  # 32 row blocks: enough for an order table
+    ref = None
+    for perm, items in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
+        monkeypatch.setenv("SILT_ROW_PERM", perm)
+        monkeypatch.setenv("SILT_WARP_ITEMS", items)
+        out, st, n, log = N.run(p, init, max_steps=steps, variant=abi.VARIANT_FAST)
+        assert n == steps
+        if ref is None:
+            ref = (out, log)
+        else:
+            assert np.array_equal(log, ref[1]), (perm, items)
+            assert np.array_equal(out, ref[0]), (perm, items)
+
+
 @pytest.mark.parametrize("case", ["C1", "C2", "periodic_ring1d"])
 @pytest.mark.parametrize("resident", ["0", "1"])
 def test_1d_cluster_kernels(N, golden, monkeypatch, case, resident):
