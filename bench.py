@@ -441,12 +441,28 @@ def main():
     per_gpu_cells = cells / world
     achieved = per_gpu_cells * BYTES_PER_CELL / (ms_step / 1e3) / 1e9
     traffic = None
+    fp64_roof = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
         tr = tj.get(args.workload)
         if tr:
             traffic = tr["dram_bytes_per_launch"] * (per_gpu_cells / tr["cells"])
+        # Active flow is bound by the FP64 pipe, not HBM: FP64-pipe thread
+        # instructions per cell-update (DFMA+DMUL+DADD+DSETP, from the committed
+        # ncu capture of this workload) x cell-updates/s, against the measured
+        # DFMA rate (profiles/r1_fp64_peak.json; one FP64-pipe instruction each).
+        with open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")) as fh:
+            fp_peak = float(json.load(fh)["dfma_per_s"])
+        if tr and tr.get("fp64_pipe_inst_per_cell") and args.variant == "fast":
+            per_cell = tr["fp64_pipe_inst_per_cell"]
+            ach = per_gpu_cells / (ms_step / 1e3) * per_cell
+            fp64_roof = {"bound": "fp64", "achieved": ach / 1e12, "peak": fp_peak / 1e12,
+                         "unit": "T FP64-pipe thread instr/s", "frac": ach / fp_peak,
+                         "per_cell": per_cell,
+                         "source": "profiles/" + tr.get("source", "?") + " opcode mix ("
+                                   + tr.get("capture", "one step launch") + "); peak "
+                                   "profiles/r1_fp64_peak.json"}
     except Exception:
         pass
 
@@ -533,6 +549,7 @@ def main():
                          "note": "algorithmic 64 B/cell-update / device time per step (the step "
                                  "kernel plus, in launches >= 64 CTAs/SM, the 1-CTA "
                                  "rb_order_kernel that orders the next launch, ~0.1 %)"},
+            "roofline_fp64": fp64_roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

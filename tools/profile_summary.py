@@ -148,6 +148,16 @@ def main():
                 tj[a.workload] = entry
                 json.dump(tj, open(tp, "w"), indent=1)
             mix = opcode_mix(a.full)
+            if mix and a.cells:
+                # FP64-pipe thread instructions per cell-update (DFMA/DMUL/DADD/DSETP),
+                # for bench.py's roofline_fp64 (the active path's binding roof)
+                k = "smsp__thread_inst_executed_per_inst_executed.ratio"
+                lanes = float(res[k][1]) if k in res else 32.0
+                fp = sum(v for op, v in mix if op in ("DFMA", "DMUL", "DADD", "DSETP"))
+                tp = os.path.join(os.path.dirname(a.out) or ".", "traffic.json")
+                tj = json.load(open(tp)) if os.path.exists(tp) else {}
+                tj.setdefault(a.workload, {})["fp64_pipe_inst_per_cell"] = lanes * fp / a.cells
+                json.dump(tj, open(tp, "w"), indent=1)
             if mix:
                 tot = sum(v for _, v in mix)
                 fp64 = sum(v for op, v in mix if op in ("DFMA", "DMUL", "DADD", "DSETP"))
