@@ -581,7 +581,19 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         const char* pe = std::getenv("SILT_ROW_PERM");
         const bool order0 = problem->dim == 2 && nb0 >= 16 && (pe ? pe[0] != '0' : ctas0 >= 64LL * nsm);
         const bool neighbours = st.south_neighbor || st.north_neighbor;
-        if (order0 && !neighbours && !(wi_env && wi_env[0] == '0')) R = std::min(R, 64LL);
+        if (order0 && !neighbours && !(wi_env && wi_env[0] == '0')) {
+            if (variant == SILT_VARIANT_STRICT) {
+                // STRICT skips a repeated row only after three full rows at
+                // the start of every row block (its repeated-row skip needs
+                // four equal rows and a computed one to repeat), so long
+                // blocks: C4 8.74 (64 rows) / 8.07 (128) / 7.45 (256) /
+                // 9.04 (384, hot blocks become the tail) ms per step
+                R = 256;
+                while (R > 64 && (s->ny + R - 1) / R < 16) R /= 2;
+            } else {
+                R = std::min(R, 64LL);
+            }
+        }
     }
     if (const char* e = std::getenv("SILT_ROWS")) R = std::max(1LL, std::atoll(e));
     if (problem->dim == 1) R = 1;

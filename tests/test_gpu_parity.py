@@ -499,10 +499,12 @@ def test_c5_size_properties(N):
     assert np.all(normwise(fo, so) <= FIELD_TOL)
 
 
+@pytest.mark.parametrize("variant", [abi.VARIANT_FAST, abi.VARIANT_STRICT])
 @pytest.mark.parametrize("case", ["C3", "C4s", "bc_inflow_wall"])
-def test_quiet_row_skip_is_bit_identical(N, golden, case, monkeypatch):
-    """The quiescent-row skip of the FAST step kernel changes no bit: runs with
-    SILT_QUIET_SKIP=0 (full path everywhere) and =1 agree exactly."""
+def test_quiet_row_skip_is_bit_identical(N, golden, case, variant, monkeypatch):
+    """The quiescent-row skip of the FAST step kernel (and the repeated-row
+    skip of the STRICT one) changes no bit: runs with SILT_QUIET_SKIP=0 (full
+    path everywhere) and =1 agree exactly."""
     if case == "C3":
         p, init, _ = scenarios.dune_2d(1024)
         steps = 300
@@ -516,10 +518,41 @@ def test_quiet_row_skip_is_bit_identical(N, golden, case, monkeypatch):
     outs = []
     for flag in ("0", "1"):
         monkeypatch.setenv("SILT_QUIET_SKIP", flag)
-        outs.append(N.run(p, init, max_steps=steps, variant=abi.VARIANT_FAST))
+        outs.append(N.run(p, init, max_steps=steps, variant=variant))
     assert outs[0][2] == outs[1][2] == steps
     assert np.array_equal(outs[0][3], outs[1][3])
     assert np.array_equal(outs[0][0], outs[1][0])
+
+
+@pytest.mark.parametrize("bcs", ["outflow", "periodic_y"])
+def test_strict_repeated_rows_match_reference(N, restatement, monkeypatch, bcs):
+    """STRICT's repeated-row skip on a flow that varies across x but not
+    along y (a bed ridge parallel to y: every row repeats, none is uniform,
+    so FAST's quiescent test never fires while STRICT's does on every row):
+    bitwise equal to the restatement (= the reference) and to the full path,
+    dt log included; then a y-bump breaks the repetition in the middle."""
+    nx, ny, steps = 157, 120, 40
+    x = np.arange(nx) + 0.5
+    zb_x = 0.1 + 0.2 * np.exp(-((x - 60.0) / 9.0) ** 2)
+    init = np.zeros((ny, nx, 4))
+    init[..., 3] = zb_x[None, :]
+    init[..., 0] = 1.8 - init[..., 3]
+    init[..., 1] = 0.9
+    init[70:74, 100:110, 3] += 0.05  # a bump: rows 70..73 differ
+    init[70:74, 100:110, 0] -= 0.05
+    p = abi.make_problem(2, nx, ny, 1.0, 1.0, a_g=0.02, cfl=0.45)
+    if bcs == "periodic_y":
+        p.bc[abi.SOUTH] = p.bc[abi.NORTH] = abi.bc("periodic")
+    ref, t, n, log = restatement.run(p, init, max_steps=steps)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SILT_QUIET_SKIP", flag)
+        monkeypatch.setenv("SILT_ROWS", "40")  # long row blocks: long repeats
+        outs.append(N.run(p, init, max_steps=steps, variant=abi.VARIANT_STRICT))
+    for out, st, sn, slog in outs:
+        assert sn == n and st == t
+        assert np.array_equal(slog, log)
+        assert np.array_equal(out, ref)
 
 
 @pytest.mark.parametrize("items", ["0", "1"])
@@ -580,8 +613,9 @@ def _bump_field(nx, ny, cx, cy, r):
     return init
 
 
+@pytest.mark.parametrize("variant", [abi.VARIANT_FAST, abi.VARIANT_STRICT])
 @pytest.mark.parametrize("bcs", ["outflow", "periodic_x_wall_y", "inflow_wall"])
-def test_streak_loop_is_bit_identical(N, monkeypatch, bcs):
+def test_streak_loop_is_bit_identical(N, monkeypatch, bcs, variant):
     """The quiescent-row skip and its streak loop (FAST) change no bit on a
     grid whose width is no multiple of the 30-column warp bands, with the
     bump near a corner (streaks begin and end at strip edges, the first and
@@ -600,14 +634,14 @@ def test_streak_loop_is_bit_identical(N, monkeypatch, bcs):
     ref = None
     for flag in ("0", "1"):
         monkeypatch.setenv("SILT_QUIET_SKIP", flag)
-        out, st, n, log = N.run(p, init, max_steps=steps, variant=abi.VARIANT_FAST)
+        out, st, n, log = N.run(p, init, max_steps=steps, variant=variant)
         assert n == steps
         if ref is None:
             ref = (out, log)
         else:
             assert np.array_equal(log, ref[1])
             assert np.array_equal(out, ref[0])
-        g = LocalStripGroup(p, 3, devices=(0,), variant=abi.VARIANT_FAST)
+        g = LocalStripGroup(p, 3, devices=(0,), variant=variant)
         g.upload(init)
         g.begin(max_steps=steps)
         g.run(batch=8)
