@@ -96,6 +96,17 @@ def main():
     ref = orc.run(p, u, max_steps=6)[0]
     check("2d quiescent fast", native.run(p, u, max_steps=6, variant=abi.VARIANT_FAST)[0], ref,
           False)
+    # repeated rows (STRICT skip + streak loop), long row blocks
+    os.environ["SILT_ROWS"] = "40"
+    check("2d repeated rows strict", native.run(p, u, max_steps=6, variant=abi.VARIANT_STRICT)[0],
+          ref, True)
+    # warp items through the row-block order table (forced on a small grid)
+    os.environ.update(SILT_ROWS="8", SILT_ROW_PERM="1", SILT_WARP_ITEMS="1")
+    for vname, v in (("strict", abi.VARIANT_STRICT), ("fast", abi.VARIANT_FAST)):
+        check(f"2d ordered warp items {vname}", native.run(p, u, max_steps=6, variant=v)[0], ref,
+              v == abi.VARIANT_STRICT)
+    for k in ("SILT_ROWS", "SILT_ROW_PERM", "SILT_WARP_ITEMS"):
+        os.environ.pop(k)
     # 1D: single launches, resident cluster (<= 8 CTAs), global-memory cluster,
     # cooperative grid
     for nx in (37, 2000, 4000, 6100):
