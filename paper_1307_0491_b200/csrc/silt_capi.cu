@@ -202,6 +202,7 @@ struct silt_solver {
     bool begun = false;
     StepArgs args{};
     dim3 step_grid;
+    dim3 row_grid;  // the launch grid (column groups x row blocks), also in warp-item mode
     // WorkerTiming split (silt_solver_timing): device time of this strip's
     // step launches, bracketed by events and harvested when the stream syncs
     bool timing_on = false;
@@ -351,6 +352,9 @@ void launch_step(silt_solver* s, int part = 0) {
     if (part == 0) {
         a.rb_map = a.rb_order ? a.rb_table[li] : nullptr;
     } else {
+        // split edge / interior launches: always on the launch grid
+        grid = s->row_grid;
+        a.warp_items = 0;
         a.rb_map = part == 1 ? s->split_map : s->split_map + 2;
         a.epilogue = part == 1 ? 1 : 0;
         grid.y = part == 1 ? 2u : grid.y - 2u;
@@ -580,8 +584,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         const long long ctas0 = nb0 * ((strips + kStepThreads / 32 - 1) / (kStepThreads / 32));
         const char* pe = std::getenv("SILT_ROW_PERM");
         const bool order0 = problem->dim == 2 && nb0 >= 16 && (pe ? pe[0] != '0' : ctas0 >= 64LL * nsm);
-        const bool neighbours = st.south_neighbor || st.north_neighbor;
-        if (order0 && !neighbours && !(wi_env && wi_env[0] == '0')) {
+        if (order0 && !(wi_env && wi_env[0] == '0')) {
             if (variant == SILT_VARIANT_STRICT) {
                 // STRICT skips a repeated row only after three full rows at
                 // the start of every row block (its repeated-row skip needs
@@ -618,14 +621,15 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         const char* e = std::getenv("SILT_ROW_PERM");
         const bool order = problem->dim == 2 && nb >= 16 && (e ? e[0] != '0' : ctas >= 64LL * sms);
         s->step_grid = dim3((unsigned)((strips + warps_per_cta - 1) / warps_per_cta), nb, 1);
+        s->row_grid = s->step_grid;
         A.rb_order = order ? 1 : 0;
         A.epilogue = 1;
         A.rb_map = nullptr;
         // Warp-item mode for short 2D launches (a few waves of CTAs, e.g. C3)
         // and long ordered ones (C4): one wave of resident CTAs whose warps
-        // pull (band, row block) items from a counter.  Not with neighbour
-        // strips (edge rows first, split launches).  SILT_WARP_ITEMS=0/1
-        // forces it off/on.
+        // pull (band, row block) items from a counter.  The split edge /
+        // interior launches of the collective multi-rank path keep the launch
+        // grid (launch_step).  SILT_WARP_ITEMS=0/1 forces it off/on.
         A.warp_items = 0;
         A.bands = (int)strips;
         A.n_items = (int)(strips * nb);
@@ -633,10 +637,11 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
         {
             const double waves = (double)ctas / ((double)ctas_per_sm * sms);
             const char* we = std::getenv("SILT_WARP_ITEMS");
+            // (short launches of strips with neighbours keep the grid: the
+            // hot piece of a two-piece rank at N = 8 measured 0.424 -> 0.460 ms)
             const bool neighbours = st.south_neighbor || st.north_neighbor;
-            bool wi = problem->dim == 2 && !neighbours &&
-                      (order || (waves <= 8.0 && waves > 1.0));
-            if (we) wi = problem->dim == 2 && !neighbours && we[0] == '1';
+            bool wi = problem->dim == 2 && (order || (waves <= 8.0 && waves > 1.0 && !neighbours));
+            if (we) wi = problem->dim == 2 && we[0] == '1';
             if (wi) {
                 const unsigned grid = (unsigned)std::min<long long>(
                     ctas, (long long)ctas_per_sm * sms);
@@ -645,8 +650,7 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
                 A.warps_total = (int)grid * warps_per_cta;
             }
         }
-        if (!A.warp_items && !order && problem->dim == 2 && nb >= 3 &&
-            (st.south_neighbor || st.north_neighbor)) {
+        if (!order && problem->dim == 2 && nb >= 3 && (st.south_neighbor || st.north_neighbor)) {
             std::vector<int> m{0, (int)nb - 1};
             for (unsigned k = 1; k + 1 < nb; ++k) m.push_back((int)k);
             if (cudaMalloc(&s->split_map, m.size() * sizeof(int)) != cudaSuccess)
