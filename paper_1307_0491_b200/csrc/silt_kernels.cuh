@@ -537,6 +537,12 @@ __device__ __forceinline__ void sides_of(const StepArgs& A, const double c[4], S
     }
 }
 
+// SILT_PDL: 2D step launches with programmatic stream serialization (the next
+// step's CTAs launch during this step's tail and wait in griddepcontrol.wait):
+// C3 74.7 -> 73.1 us per step, bit-identical; long launches unchanged
+#ifndef SILT_PDL
+#define SILT_PDL 1
+#endif
 // SILT_RING: cp.async ring slots; rows are issued SILT_RING-1 ahead
 // Per-CTA shared memory of the 2D step (dynamic: above the 48 KB static cap).
 struct StepSmem {
@@ -560,6 +566,14 @@ __global__ void __launch_bounds__(kStepThreads, SILT_STEP_MIN_BLOCKS) step2d_ker
     // so that registers at each face solve hold little beyond the solver.
     extern __shared__ __align__(16) unsigned char step_smem_raw[];
     StepSmem& sm = *reinterpret_cast<StepSmem*>(step_smem_raw);
+#if SILT_PDL
+    // Programmatic dependent launch: this grid may be launched while the
+    // previous step's is still finishing; wait for it (and its memory) before
+    // touching the control slot or the state, and let the next step's grid
+    // launch as soon as every CTA of this one is running.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
     auto& sh_side = sm.side;
     auto& sh_sx = sm.sx;
     auto& sh_xs = sm.xs;
@@ -1348,7 +1362,24 @@ __global__ void law_batch_kernel(Params P, const double* X, long long n, double*
                                          std::atoi(cv));                                         \
                 attr_set |= 1ull << (dev_ & 63);                                                 \
             }                                                                                    \
-            if (A.warp_items)                                                                    \
+            if (SILT_PDL) {                                                                      \
+                cudaLaunchConfig_t cfg{};                                                        \
+                cfg.gridDim = grid;                                                              \
+                cfg.blockDim = dim3(kStepThreads);                                               \
+                cfg.dynamicSmemBytes = sizeof(silt_dev::StepSmem);                               \
+                cfg.stream = st;                                                                 \
+                cudaLaunchAttribute at[1];                                                       \
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                   \
+                at[0].val.programmaticStreamSerializationAllowed = 1;                            \
+                cfg.attrs = at;                                                                  \
+                cfg.numAttrs = 1;                                                                \
+                StepArgs a_ = A;                                                                 \
+                int li_ = li;                                                                    \
+                if (A.warp_items)                                                                \
+                    cudaLaunchKernelEx(&cfg, silt_dev::step2d_kernel<S, SH, true>, a_, li_);     \
+                else                                                                             \
+                    cudaLaunchKernelEx(&cfg, silt_dev::step2d_kernel<S, SH, false>, a_, li_);    \
+            } else if (A.warp_items)                                                             \
                 silt_dev::step2d_kernel<S, SH, true>                                             \
                     <<<grid, kStepThreads, sizeof(silt_dev::StepSmem), st>>>(A, li);             \
             else                                                                                 \
