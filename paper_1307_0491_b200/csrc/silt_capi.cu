@@ -590,7 +590,10 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
                 // the start of every row block (its repeated-row skip needs
                 // four equal rows and a computed one to repeat), so long
                 // blocks: C4 8.74 (64 rows) / 8.07 (128) / 7.45 (256) /
-                // 9.04 (384, hot blocks become the tail) ms per step
+                // 9.04 (384, hot blocks become the tail) ms per step.  At 256
+                // rows C4 is 64 x 137 CTAs, below the ordered-launch size:
+                // the launch grid in row order (forcing the order table,
+                // with or without warp items: 8.35 ms over 100 steps).
                 R = 256;
                 while (R > 64 && (s->ny + R - 1) / R < 16) R /= 2;
             } else {
