@@ -2,11 +2,15 @@
 by the REFERENCE itself (oracle/_ref/libsilt_ref.so, its own scenario
 builders and run_serial):
 
-  3  dune migration + refinement  (proj/tests/acceptance_main.cpp:164-195)
-  4  antidune upstream migration  (:199-225)
-  10 planar bump crescent         (:419-449)
+  1  periodic dune conserves water and bed  (proj/tests/acceptance_main.cpp:104-126)
+  2  dam break = plain shallow water         (:130-160)
+  3  dune migration + refinement             (:164-195)
+  4  antidune upstream migration             (:199-225)
+  9  lake at rest: spurious |u| shrinks      (:395-415)
+  10 planar bump crescent                    (:419-449)
 
     make -C oracle && python tests/golden/make_golden_acceptance.py   (~10 min)
+    python tests/golden/make_golden_acceptance.py --extra   (criteria 1, 2, 9 only; merged)
 
 tests/test_acceptance.py runs the same scenarios on the GPU path and compares
 the crest tracks, bed L1 gaps, inflow Froude numbers and bed maxima with
@@ -78,9 +82,90 @@ def bump_split(field):
     return float(centre), float(off)
 
 
+def conservation_case(R):
+    """Criterion 1's scenario: dune1d(500) between periodic ends, 1000 steps."""
+    from paper_1307_0491_b200 import abi
+    p, init, _ = R.build_scenario("dune1d", 500)
+    p.bc[abi.WEST] = abi.bc("periodic")
+    p.bc[abi.EAST] = abi.bc("periodic")
+    return p, init
+
+
+def volumes(f, dx):
+    """water_volume / bed_volume (acceptance_main.cpp:49-59), summed in cell order."""
+    w = b = 0.0
+    for c in f.reshape(-1, 4):
+        w += float(c[0])
+        b += float(c[3])
+    return w * dx, b * dx
+
+
+def dam_break_case():
+    """Criterion 2's scenario: 400 cells on [0, 200] m, h = 2 | 1 at x = 100,
+    no transport (Grass A_g = 0), t_end = 10 s, transmissive ends."""
+    from paper_1307_0491_b200 import abi
+    n = 400
+    p = abi.make_problem(1, n, 1, 200.0 / n, 1.0, a_g=0.0, cfl=0.5)
+    f = np.zeros((1, n, 4))
+    x = (np.arange(n) + 0.5) * (200.0 / n)
+    f[0, :, 0] = np.where(x < 100.0, 2.0, 1.0)
+    return p, f, 10.0
+
+
+def lake_case(R, cells):
+    """Criterion 9's scenario: dune1d(cells) with Grass A_g = 0, walls, hu = 0, t_end = 20."""
+    from paper_1307_0491_b200 import abi
+    p, init, _ = R.build_scenario("dune1d", cells)
+    p.a_g = 0.0
+    p.bc[abi.WEST] = abi.bc("wall")
+    p.bc[abi.EAST] = abi.bc("wall")
+    init = init.copy()
+    init[..., 1] = 0.0
+    return p, init, 20.0
+
+
+def umax(f):
+    return float(np.max(np.abs(f[..., 1] / f[..., 0])))
+
+
+def extra(R):
+    """Criteria 1, 2, 9 on the reference (run_serial through oracle/_ref)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import kats
+    out = {}
+    p, init = conservation_case(R)
+    f, t, steps, _ = R.run(p, init, t_end=1e6, max_steps=1000)
+    w0, b0 = volumes(init, p.dx)
+    w1, b1 = volumes(f, p.dx)
+    out["conservation"] = {"steps": steps, "water_drift": abs(w1 - w0) / w0,
+                           "bed_drift": abs(b1 - b0) / b0}
+    p, f0, t_end = dam_break_case()
+    f, t, steps, _ = R.run(p, f0, t_end=t_end)
+    rh, rhu = kats.suliciu_run(f0[0, :, 0], f0[0, :, 1], p.dx, t_end)
+    gap = max(float(np.max(np.abs(f[0, :, 0] - rh))), float(np.max(np.abs(f[0, :, 1] - rhu))))
+    out["dam_break"] = {"t": t, "steps": steps, "gap": gap,
+                        "bed_clean": bool(np.all(f[..., 3] == 0.0))}
+    lake = {}
+    for cells in (500, 1000):
+        p, init, t_end = lake_case(R, cells)
+        f, t, steps, _ = R.run(p, init, t_end=t_end)
+        lake[str(cells)] = {"umax": umax(f), "steps": steps, "t": t}
+    out["lake"] = lake
+    return out
+
+
 def main():
     import oracle as O
     R = O.reference()
+    if "--extra" in sys.argv:
+        path = os.path.join(HERE, "golden_acceptance.json")
+        with open(path) as fh:
+            out = json.load(fh)
+        out.update(extra(R))
+        print({k: out[k] for k in ("conservation", "dam_break", "lake")}, flush=True)
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+        return
 
     def dune(cells):
         p, init, t_end = R.build_scenario("dune1d", cells)
@@ -117,6 +202,7 @@ def main():
     out["bump"] = {"t_end": t_end, "steps": steps, "centre0": c0, "off0": o0, "centre1": c1,
                    "off1": o1, "lowered": c1 < c0, "split": o1 > c1}
     print("bump", out["bump"], flush=True)
+    out.update(extra(R))
     with open(os.path.join(HERE, "golden_acceptance.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 

@@ -1,8 +1,11 @@
 """The reference's physics acceptance criteria through the GPU path.
 
-  3  dune migration + refinement  (proj/tests/acceptance_main.cpp:164-195)
-  4  antidune upstream migration  (:199-225)
-  10 planar bump crescent         (:419-449)
+  1  periodic dune conserves water and bed  (proj/tests/acceptance_main.cpp:104-126)
+  2  dam break = plain shallow water         (:130-160)
+  3  dune migration + refinement             (:164-195)
+  4  antidune upstream migration             (:199-225)
+  9  lake at rest: spurious |u| shrinks      (:395-415)
+  10 planar bump crescent                    (:419-449)
 
 Inputs come from the reference's own scenario builders (oracle/_ref, test
 infrastructure; build_dune_1d / build_antidune_1d / build_bump_2d), the runs
@@ -106,3 +109,65 @@ def test_bump_crescent(ref, expected):
     assert math.isclose(c1, e["centre1"], rel_tol=1e-9)
     assert math.isclose(o1, e["off1"], rel_tol=1e-9)
     assert (c1 < c0) == e["lowered"] and (o1 > c1) == e["split"]
+
+
+def _variants():
+    from paper_1307_0491_b200 import abi
+    return (("strict", abi.VARIANT_STRICT), ("fast", abi.VARIANT_FAST))
+
+
+def test_conservation_periodic_dune(ref, expected):
+    """Criterion 1: the dune between periodic ends, 1000 steps: relative water
+    and bed drift below 1e-12 (STRICT: the reference's own drifts, bit for bit)."""
+    from paper_1307_0491_b200 import native
+    e = expected["conservation"]
+    p, init = A.conservation_case(ref)
+    w0, b0 = A.volumes(init, p.dx)
+    for name, v in _variants():
+        f, t, steps, _ = native.run(p, init, t_end=1e6, max_steps=1000, variant=v)
+        w1, b1 = A.volumes(f, p.dx)
+        dw, db = abs(w1 - w0) / w0, abs(b1 - b0) / b0
+        print(f"GPU {name} conservation: water drift {dw:.2e}, bed drift {db:.2e}; reference", e)
+        assert steps == e["steps"] == 1000 and dw < 1e-12 and db < 1e-12
+        if name == "strict":
+            assert dw == e["water_drift"] and db == e["bed_drift"]
+
+
+def test_dam_break_is_shallow_water(expected):
+    """Criterion 2: with transport off the scheme is plain shallow water: within
+    1e-12 of an independent Suliciu solver (tests/kats.py), bed bit-unchanged."""
+    import kats
+    from paper_1307_0491_b200 import native
+    e = expected["dam_break"]
+    p, f0, t_end = A.dam_break_case()
+    rh, rhu = kats.suliciu_run(f0[0, :, 0], f0[0, :, 1], p.dx, t_end)
+    for name, v in _variants():
+        f, t, steps, _ = native.run(p, f0, t_end=t_end, variant=v)
+        gap = max(float(np.max(np.abs(f[0, :, 0] - rh))), float(np.max(np.abs(f[0, :, 1] - rhu))))
+        print(f"GPU {name} dam break: gap {gap:.2e} after {steps} steps; reference", e)
+        assert t == e["t"] == t_end and steps == e["steps"]
+        assert gap <= 1e-12 and np.all(f[..., 3] == 0.0)
+        if name == "strict":
+            assert gap == e["gap"]
+
+
+def test_lake_at_rest(ref, expected):
+    """Criterion 9: a flat free surface over the dune with transport off, walls
+    at both ends, to t = 20 s: the spurious velocity is nonzero and shrinks
+    from 500 to 1000 cells — the reference's own values (STRICT bit for bit)."""
+    from paper_1307_0491_b200 import native
+    e = expected["lake"]
+    for name, v in _variants():
+        um = {}
+        for cells in (500, 1000):
+            p, init, t_end = A.lake_case(ref, cells)
+            f, t, steps, _ = native.run(p, init, t_end=t_end, variant=v)
+            assert t == t_end and steps == e[str(cells)]["steps"]
+            um[cells] = A.umax(f)
+            want = e[str(cells)]["umax"]
+            if name == "strict":
+                assert um[cells] == want
+            else:
+                assert math.isclose(um[cells], want, rel_tol=1e-9)
+        print(f"GPU {name} lake at rest: max |u| {um[500]:.3e} (500) -> {um[1000]:.3e} (1000)")
+        assert um[500] > 1e-14 and um[1000] > 1e-14 and um[1000] < um[500]
