@@ -570,12 +570,13 @@ int silt_solver_create(const silt_problem* problem, const silt_strip* strip, int
             if (waste(cand) < waste(best) - 0.05) best = cand;
         R = best;
     }
-    // Long launches of one strip (the row-block order below applies) run as
-    // warp items too (warps pull (band, row block) items through the order
+    // Long launches (those the row-block order below applies to) run as warp
+    // items too (FAST: warps pull (band, row block) items through the order
     // table, no CTA start-up per block and no warp slot held by a finished
-    // warp of a hot CTA), with row blocks of at most 64 rows: C4 3.004 ->
+    // warp of a hot CTA) with row blocks of at most 64 rows: C4 3.004 ->
     // 2.958 ms per step (20 steps; ~neutral over 500 steps, where the faster
-    // kernel meets the power cap), the uniform field unchanged.
+    // kernel meets the power cap), the uniform field unchanged, a 2-strip
+    // half 1.526 -> 1.497 ms.  STRICT: see below.
     const char* wi_env = std::getenv("SILT_WARP_ITEMS");
     {
         int nsm = 148;
