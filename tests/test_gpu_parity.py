@@ -660,6 +660,7 @@ def test_launch_orders_are_bit_identical(N, monkeypatch):
     init = _bump_field(nx, ny, 160.0, 120.0, 30.0)
     p = abi.make_problem(2, nx, ny, 1.0, 1.0, a_g=0.01, cfl=0.45)
     monkeypatch.setenv("SILT_ROWS", "8")  # 32 row blocks: enough for an order table
+    from paper_1307_0491_b200.distributed import LocalStripGroup
     ref = None
     for perm, items in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
         monkeypatch.setenv("SILT_ROW_PERM", perm)
@@ -671,6 +672,14 @@ def test_launch_orders_are_bit_identical(N, monkeypatch):
         else:
             assert np.array_equal(log, ref[1]), (perm, items)
             assert np.array_equal(out, ref[0]), (perm, items)
+        # the same orders on strips with neighbours (edge rows into the
+        # neighbours' receive rows from whichever warp holds the edge block)
+        g = LocalStripGroup(p, 2, devices=(0,), variant=abi.VARIANT_FAST)
+        g.upload(init)
+        g.begin(max_steps=steps)
+        g.run(batch=8)
+        assert np.array_equal(g.gather(), ref[0]), ("strips", perm, items)
+        g.close()
 
 
 @pytest.mark.parametrize("case", ["C1", "C2", "periodic_ring1d"])
